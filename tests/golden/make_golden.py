@@ -1,0 +1,200 @@
+"""Generate the golden vectors under tests/golden/ FROM THE REFERENCE ITSELF.
+
+Runs the unmodified reference package (``beamoe``, built into ``oracle/_ref``
+by ``oracle/build_ref.sh`` from /root/reference/pkg) on seeded inputs and
+stores inputs + outputs as compressed ``.npz`` fixtures.  Only needs to run in
+the build container (the GPU box has no /root/reference); the fixtures are
+committed.
+
+    python tests/golden/make_golden.py
+
+Cases
+-----
+mask_route_*      — dispatch.mask_route (dispatch/__init__.py:55-62)
+align_*           — dispatch.align_block (dispatch/__init__.py:89-126), many block sizes
+topk_*            — moe.topk_route incl. ties (moe.py:116-137)
+layer_*           — beam.beam_block_forward(training=False) (beam.py:127-165)
+                    on small random blocks (norm / shared / non-zero mask router)
+q30route_dyadic   — Qwen3-30B-A3B router shape (N=128, K=8, d=2048), dyadic inputs,
+                    so logits / pre-activations are exact in fp32 and fp64: top-K ids,
+                    mask bits and the plan must match bit-for-bit.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import ref  # noqa: E402
+
+
+def _plan_arrays(plan):
+    offs = np.zeros(plan.num_experts + 1, dtype=np.int64)
+    for e in range(plan.num_experts):
+        offs[e + 1] = offs[e] + plan.padded_count(e)
+    tokens = np.concatenate([np.asarray(t, dtype=np.int64) for t in plan.tokens]) if plan.num_experts else np.zeros(0, np.int64)
+    slots = np.concatenate([np.asarray(s, dtype=np.int64) for s in plan.slots]) if plan.num_experts else np.zeros(0, np.int64)
+    return dict(plan_counts=np.asarray(plan.real_counts, dtype=np.int64), plan_offsets=offs,
+                plan_tokens=tokens, plan_slots=slots, plan_block_size=np.int64(plan.block_size))
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
+def main():
+    beamoe = ref.import_beamoe()
+    from beamoe import dispatch
+    from beamoe.beam import MaskRouter, beam_block_forward
+    from beamoe.moe import MoEBlock, MoEBlockConfig, topk_route
+    from beamoe.tensor import Tensor
+
+    # ---------------- mask_route ----------------
+    rng = np.random.default_rng(1000)
+    cases = []
+    # reference KATs (test_dispatch.py:35-53)
+    a = np.zeros((1, 8)); a[0, 3] = 0.2; a[0, 5] = -0.1
+    cases.append((np.array([[3, 5]], np.int64), a))
+    cases.append((np.array([[0, 1], [2, 3]], np.int64), np.zeros((2, 4))))
+    cases.append((np.array([[-1, 7, 2]], np.int64), np.zeros((1, 4))))
+    # signed zeros + exact boundary
+    cases.append((np.array([[0, 1, 2, 3]], np.int64), np.array([[0.0, -0.0, 1e-300, -1e-300]])))
+    for _ in range(20):
+        t, k, n = int(rng.integers(1, 40)), int(rng.integers(1, 9)), int(rng.integers(2, 130))
+        ids = rng.integers(-2, n + 2, (t, k)).astype(np.int64)
+        cases.append((ids, rng.normal(size=(t, n))))
+    arrays = {}
+    for i, (ids, a) in enumerate(cases):
+        arrays[f"ids_{i}"] = ids
+        arrays[f"a_{i}"] = a
+        arrays[f"out_{i}"] = dispatch.mask_route(ids, a)
+    arrays["n_cases"] = np.int64(len(cases))
+    save("mask_route", **arrays)
+
+    # ---------------- align_block ----------------
+    rng = np.random.default_rng(2000)
+    arrays = {}
+    specs = [(np.array([[0, 1], [1, -1]], np.int64), 2, 2), (np.full((5, 3), -1, np.int64), 16, 4)]
+    for bs in (1, 2, 4, 8, 16, 64):
+        for _ in range(3):
+            n = int(rng.integers(1, 130))
+            t, k = int(rng.integers(1, 300)), int(rng.integers(1, 9))
+            specs.append((rng.integers(-1, n, (t, k)).astype(np.int64), bs, n))
+    for i, (ids, bs, n) in enumerate(specs):
+        plan = dispatch.align_block(ids, bs, num_experts=n)
+        arrays[f"ids_{i}"] = ids
+        arrays[f"bs_{i}"] = np.int64(bs)
+        arrays[f"n_{i}"] = np.int64(n)
+        for key, v in _plan_arrays(plan).items():
+            arrays[f"{key}_{i}"] = v
+    arrays["n_cases"] = np.int64(len(specs))
+    save("align_block", **arrays)
+
+    # ---------------- topk_route ----------------
+    rng = np.random.default_rng(3000)
+    arrays = {}
+    topk_cases = [
+        (np.array([[2.0, 1.0, 0.0, -1.0]]), np.eye(4), 2),      # test_moe.py:64-73
+        (np.array([[1.0, 1.0, 1.0, 1.0]]), np.eye(4), 2),       # ties -> lowest index
+        (np.array([[5.0, 5.0, 5.0]]), np.eye(3), 2),
+        (rng.normal(size=(5, 4)), rng.normal(size=(4, 6)), 6),  # K = N
+    ]
+    for _ in range(6):
+        t, d, n = int(rng.integers(1, 20)), int(rng.integers(1, 40)), int(rng.integers(2, 130))
+        k = int(rng.integers(1, min(n, 8) + 1))
+        topk_cases.append((rng.normal(size=(t, d)), rng.normal(size=(d, n)), k))
+    # many exact ties: small-integer logits
+    topk_cases.append((rng.integers(-2, 3, (64, 16)).astype(np.float64), np.eye(16), 8))
+    for i, (x, w, k) in enumerate(topk_cases):
+        dec = topk_route(Tensor(x), Tensor(w), k)
+        arrays[f"x_{i}"] = x
+        arrays[f"w_{i}"] = w
+        arrays[f"k_{i}"] = np.int64(k)
+        arrays[f"logits_{i}"] = dec.logits.data
+        arrays[f"ids_{i}"] = dec.topk_indices
+        arrays[f"weights_{i}"] = dec.weights.data
+    arrays["n_cases"] = np.int64(len(topk_cases))
+    save("topk_route", **arrays)
+
+    # ---------------- full layer, inference ----------------
+    arrays = {}
+    layer_specs = [
+        # (seed, d, f, n, k, shared, has_norm, T, mask_std, bs)
+        (11, 32, 24, 8, 2, 0, True, 37, 1.0, 16),
+        (12, 32, 24, 8, 4, 1, True, 19, 0.5, 4),
+        (13, 16, 8, 4, 4, 0, False, 9, 0.0, 1),     # zero-init mask (== vanilla top-k)
+        (14, 48, 40, 16, 3, 2, True, 50, 2.0, 8),
+        (15, 24, 16, 6, 1, 0, True, 23, 1.0, 2),
+    ]
+    for i, (seed, d, f, n, k, sh, norm, t, mstd, bs) in enumerate(layer_specs):
+        rng = np.random.default_rng(seed)
+        cfg = MoEBlockConfig(d_h=d, d_ff=f, num_experts=n, top_k=k, num_shared=sh, has_norm=norm)
+        block = MoEBlock(cfg, rng, init_std=0.3)
+        block.mask_router = MaskRouter.zero_init(d, n)
+        if mstd > 0:
+            block.mask_router.weight.data[...] = rng.normal(0, mstd, (d, n))
+        h = rng.normal(size=(t, d))
+        out, dec, mdec = beam_block_forward(Tensor(h), block, training=False, block_size=bs)
+        masked_ids = dispatch.mask_route(dec.topk_indices, mdec.pre_activation.data)
+        plan = dispatch.align_block(masked_ids, bs, num_experts=n)
+        p = f"c{i}_"
+        arrays[p + "cfg"] = np.array([seed, d, f, n, k, sh, int(norm), t, bs], np.int64)
+        arrays[p + "h"] = h
+        arrays[p + "router_w"] = block.router_w.data
+        arrays[p + "mask_w"] = block.mask_router.weight.data
+        arrays[p + "w_gate"] = np.stack([e.w_gate.data for e in block.experts])
+        arrays[p + "w_up"] = np.stack([e.w_up.data for e in block.experts])
+        arrays[p + "w_down"] = np.stack([e.w_down.data for e in block.experts])
+        if sh:
+            arrays[p + "s_gate"] = np.stack([e.w_gate.data for e in block.shared])
+            arrays[p + "s_up"] = np.stack([e.w_up.data for e in block.shared])
+            arrays[p + "s_down"] = np.stack([e.w_down.data for e in block.shared])
+        arrays[p + "out"] = out.data
+        arrays[p + "logits"] = dec.logits.data
+        arrays[p + "topk_ids"] = dec.topk_indices
+        arrays[p + "weights"] = dec.weights.data
+        arrays[p + "pre_activation"] = mdec.pre_activation.data
+        arrays[p + "raw_mask"] = mdec.raw_mask.data
+        arrays[p + "mask"] = mdec.mask.data
+        arrays[p + "masked_ids"] = masked_ids
+        for key, v in _plan_arrays(plan).items():
+            arrays[p + key] = v
+    arrays["n_cases"] = np.int64(len(layer_specs))
+    save("layer", **arrays)
+
+    # ---------------- Q30 routing, dyadic (bit-exact suite) ----------------
+    rng = np.random.default_rng(4000)
+    d, n, k, t = 2048, 128, 8, 64
+    hq = rng.integers(-16, 17, (t, d)).astype(np.int8)          # h = hq / 8
+    rq = rng.integers(-32, 33, (d, n)).astype(np.int8)          # router = rq / 256
+    mq = rng.integers(-32, 33, (d, n)).astype(np.int8)          # mask_w = mq / 256
+    mq[:, :4] = 0                                               # a == 0 exactly: inclusive boundary
+    h = hq.astype(np.float64) / 8.0
+    router = rq.astype(np.float64) / 256.0
+    mask_w = mq.astype(np.float64) / 256.0
+    cfg = MoEBlockConfig(d_h=d, d_ff=8, num_experts=n, top_k=k, has_norm=False)
+    x = Tensor(h)
+    dec = topk_route(x, Tensor(router), k)
+    from beamoe.beam import mask_forward
+
+    mdec = mask_forward(x, MaskRouter(Tensor(mask_w)))
+    masked_ids = dispatch.mask_route(dec.topk_indices, mdec.pre_activation.data)
+    plan = dispatch.align_block(masked_ids, 16, num_experts=n)
+    arrays = dict(hq=hq, rq=rq, mq=mq, logits=dec.logits.data, topk_ids=dec.topk_indices,
+                  weights=dec.weights.data, pre_activation=mdec.pre_activation.data,
+                  mask=mdec.mask.data, masked_ids=masked_ids)
+    arrays.update(_plan_arrays(plan))
+    save("q30route_dyadic", **arrays)
+    del cfg
+
+
+if __name__ == "__main__":
+    main()

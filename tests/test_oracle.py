@@ -1,0 +1,157 @@
+"""Pin the CPU oracle (oracle/beam_oracle.py) against the reference's own
+outputs: the committed golden vectors (tests/golden/, generated from the
+reference package by tests/golden/make_golden.py) and, where oracle/_ref is
+built, live reference runs.  CPU only."""
+
+import numpy as np
+import pytest
+
+from oracle import beam_oracle as O
+from oracle import ref
+
+
+def _plan_flat(plan):
+    offs = [0]
+    for e in range(plan.num_experts):
+        offs.append(offs[-1] + plan.padded_count(e))
+    toks = np.concatenate(plan.tokens) if plan.num_experts else np.zeros(0, np.int64)
+    slots = np.concatenate(plan.slots) if plan.num_experts else np.zeros(0, np.int64)
+    return np.asarray(offs), toks, slots
+
+
+def test_mask_route_golden(golden):
+    g = golden("mask_route")
+    for i in range(int(g["n_cases"])):
+        out = O.mask_route(g[f"ids_{i}"], g[f"a_{i}"])
+        assert np.array_equal(out, g[f"out_{i}"]), i
+
+
+def test_align_block_golden(golden):
+    g = golden("align_block")
+    for i in range(int(g["n_cases"])):
+        plan = O.align_block(g[f"ids_{i}"], int(g[f"bs_{i}"]), int(g[f"n_{i}"]))
+        offs, toks, slots = _plan_flat(plan)
+        assert np.array_equal(plan.real_counts, g[f"plan_counts_{i}"]), i
+        assert np.array_equal(offs, g[f"plan_offsets_{i}"]), i
+        assert np.array_equal(toks, g[f"plan_tokens_{i}"]), i
+        assert np.array_equal(slots, g[f"plan_slots_{i}"]), i
+
+
+def test_topk_route_golden(golden):
+    g = golden("topk_route")
+    for i in range(int(g["n_cases"])):
+        dec = O.topk_route(g[f"x_{i}"], g[f"w_{i}"], int(g[f"k_{i}"]))
+        assert np.array_equal(dec.topk_indices, g[f"ids_{i}"]), i
+        assert np.array_equal(dec.logits, g[f"logits_{i}"]), i
+        np.testing.assert_allclose(dec.weights, g[f"weights_{i}"], rtol=0, atol=1e-15)
+
+
+def golden_block(g, i):
+    seed, d, f, n, k, sh, norm, t, bs = (int(v) for v in g[f"c{i}_cfg"])
+    p = f"c{i}_"
+    experts = [(g[p + "w_gate"][e], g[p + "w_up"][e], g[p + "w_down"][e]) for e in range(n)]
+    shared = [(g[p + "s_gate"][s], g[p + "s_up"][s], g[p + "s_down"][s]) for s in range(sh)]
+    block = O.OracleBlock(d_h=d, d_ff=f, num_experts=n, top_k=k, router_w=g[p + "router_w"],
+                          experts=experts, shared=shared, norm_w=np.ones(d) if norm else None,
+                          mask_w=g[p + "mask_w"])
+    return block, g[p + "h"], bs
+
+
+def test_layer_golden(golden):
+    g = golden("layer")
+    for i in range(int(g["n_cases"])):
+        block, h, bs = golden_block(g, i)
+        r = O.beam_block_forward(h, block, block_size=bs)
+        p = f"c{i}_"
+        assert np.array_equal(r.decision.topk_indices, g[p + "topk_ids"])
+        assert np.array_equal(r.masked_ids, g[p + "masked_ids"])
+        assert np.array_equal(r.mask.mask, g[p + "mask"])
+        offs, toks, slots = _plan_flat(r.plan)
+        assert np.array_equal(toks, g[p + "plan_tokens"]) and np.array_equal(slots, g[p + "plan_slots"])
+        assert np.array_equal(offs, g[p + "plan_offsets"])
+        # identical float64 arithmetic, same op order -> bit-identical
+        assert np.array_equal(r.out, g[p + "out"]), i
+        assert np.array_equal(r.decision.weights, g[p + "weights"])
+        assert np.array_equal(r.mask.raw_mask, g[p + "raw_mask"])
+
+
+def test_q30_dyadic_golden(golden):
+    g = golden("q30route_dyadic")
+    h = g["hq"].astype(np.float64) / 8
+    router = g["rq"].astype(np.float64) / 256
+    mask_w = g["mq"].astype(np.float64) / 256
+    dec = O.topk_route(h, router, 8)
+    md = O.mask_forward(h, mask_w)
+    assert np.array_equal(dec.logits, g["logits"])
+    assert np.array_equal(dec.topk_indices, g["topk_ids"])
+    assert np.array_equal(md.pre_activation, g["pre_activation"])
+    masked = O.mask_route(dec.topk_indices, md.pre_activation)
+    assert np.array_equal(masked, g["masked_ids"])
+    plan = O.align_block(masked, 16, 128)
+    offs, toks, slots = _plan_flat(plan)
+    assert np.array_equal(toks, g["plan_tokens"]) and np.array_equal(offs, g["plan_offsets"])
+    # fp32 exactness of the dyadic construction: every logit is a
+    # multiple of 2^-11 with |value| < 2^9, so float32 holds it exactly
+    for arr in (dec.logits, md.pre_activation):
+        assert np.array_equal(arr.astype(np.float32).astype(np.float64), arr)
+        assert np.array_equal(arr * 2048, np.round(arr * 2048))
+
+
+def test_grouped_equals_naive_oracle():
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        t, n, k, d, f = 16, 8, 4, 6, 5
+        ids = np.stack([rng.choice(n, size=k, replace=False) for _ in range(t)]).astype(np.int64)
+        keep = rng.random((t, k)) >= rng.uniform(0, 1)
+        masked = np.where(keep, ids, -1)
+        w = np.zeros((t, n))
+        for a in range(t):
+            for b in range(k):
+                if keep[a, b]:
+                    w[a, ids[a, b]] = rng.uniform(0.05, 1.0)
+        experts = [tuple(rng.normal(0, 0.4, s) for s in ((d, f), (d, f), (f, d))) for _ in range(n)]
+        h = rng.normal(size=(t, d))
+        plan = O.align_block(masked, int(rng.choice([1, 2, 16])), n)
+        assert np.max(np.abs(O.grouped_execute(h, plan, experts, w) - O.naive_execute(h, masked, experts, w))) < 1e-9
+
+
+def test_contract_errors():
+    with pytest.raises(O.ContractError):
+        O.align_block(np.zeros((1, 1), np.int64), 0, 1)
+    plan = O.align_block(np.array([[0]]), 1, 1)
+    e = [(np.ones((1, 1)), np.ones((1, 1)), np.ones((1, 1)))]
+    with pytest.raises(O.ContractError):
+        O.grouped_execute(np.ones((1, 1)), plan, e, np.zeros((1, 1)))
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_make_block_matches_reference_draw_order():
+    beamoe = ref.import_beamoe()
+    from beamoe.moe import MoEBlock, MoEBlockConfig
+
+    for sh in (0, 2):
+        cfg = MoEBlockConfig(d_h=12, d_ff=7, num_experts=5, top_k=2, num_shared=sh)
+        rb = MoEBlock(cfg, np.random.default_rng(3))
+        ob = O.make_block(12, 7, 5, 2, np.random.default_rng(3), num_shared=sh)
+        assert np.array_equal(rb.router_w.data, ob.router_w)
+        for re_, oe in zip(rb.experts + rb.shared, ob.experts + ob.shared):
+            assert np.array_equal(re_.w_gate.data, oe[0])
+            assert np.array_equal(re_.w_up.data, oe[1])
+            assert np.array_equal(re_.w_down.data, oe[2])
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_layer_matches_live_reference():
+    beamoe = ref.import_beamoe()
+    from beamoe.beam import beam_block_forward
+    from beamoe.tensor import Tensor
+
+    rng = np.random.default_rng(21)
+    for trial in range(5):
+        ob = O.make_block(24, 16, 8, 3, rng, num_shared=trial % 2, init_std=0.3)
+        ob.mask_w = rng.normal(0, 1.0, ob.mask_w.shape)
+        h = rng.normal(size=(13, 24))
+        out, dec, md = beam_block_forward(Tensor(h), ref.to_reference_block(ob, beamoe), training=False)
+        r = O.beam_block_forward(h, ob)
+        assert np.array_equal(out.data, r.out)
+        assert np.array_equal(dec.topk_indices, r.decision.topk_indices)
