@@ -1,0 +1,155 @@
+/*
+ * beam_b200.h — C ABI of the B200-native BEAM MoE-layer hot path.
+ *
+ * The reference (arxiv 2605.14438, package `beamoe`, /root/reference/pkg) has
+ * exactly one native plugin boundary on this path: the dispatch backend module
+ * (`beamoe.dispatch._kernels`, Cython) registered in `_BACKENDS`
+ * (src/beamoe/dispatch/__init__.py:21-44) and exposing
+ *     mask_route(topk_ids int64[T,K], mask_logits f64[T,N]) -> int64[T,K]
+ *     group_by_expert(ids int64[T,K], num_experts) -> (counts, token_order, slot_order)
+ * (src/beamoe/dispatch/_kernels.pyx:17-34, :37-66).  Everything else on the
+ * path is Python (beam.py / moe.py / dispatch/__init__.py).  This library
+ * replaces that backend AND the Python stages around it:
+ *
+ *   beam_mask_route        <- _kernels.pyx:17-34       (dispatch.mask_route, __init__.py:55-62)
+ *   beam_group_by_expert   <- _kernels.pyx:37-66 + the padding loop of
+ *                             dispatch.align_block (__init__.py:89-126)
+ *   beam_grouped_execute   <- dispatch.grouped_execute (__init__.py:129-157)
+ *                             incl. its contract checks (:143-144, :152-153)
+ *   beam_layer_forward     <- beam.beam_block_forward(training=False)
+ *                             (beam.py:127-165: rms_norm -> topk_route ->
+ *                              mask_forward -> mask_route -> align_block ->
+ *                              grouped_execute -> shared experts -> residual)
+ *   beam_gate              <- the routing half of the above (moe.topk_route
+ *                             moe.py:122-137 + beam.mask_forward beam.py:68-72
+ *                             + mask_route) = RouterDecision / MaskDecision
+ *   beam_moe_execute       <- the dispatch half of the above for externally
+ *                             supplied (masked ids, weights): used by the
+ *                             expert-parallel path on each rank.
+ *
+ * Conventions: all pointers are DEVICE pointers unless stated; every entry
+ * launches on `stream` only, never allocates, never synchronises the host, and
+ * returns BEAM_OK or a negative status.  Scratch comes from the caller's
+ * workspace (size from beam_workspace_bytes).  Results are deterministic and
+ * independent of grid size (no floating-point atomics).
+ */
+#ifndef BEAM_B200_H
+#define BEAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* beam_stream_t; /* == cudaStream_t */
+
+enum {
+  BEAM_OK = 0,
+  BEAM_ERR_ARG = -1,          /* bad pointer / size / dtype                     */
+  BEAM_ERR_UNSUPPORTED = -2,  /* shape outside what the kernels were built for  */
+  BEAM_ERR_CUDA = -3,         /* a CUDA launch failed (see beam_last_cuda_error) */
+  BEAM_ERR_WORKSPACE = -4     /* workspace smaller than beam_workspace_bytes()  */
+};
+
+enum { BEAM_F32 = 0, BEAM_BF16 = 1, BEAM_F64 = 2 };
+enum { BEAM_ACT_SILU = 0, BEAM_ACT_IDENTITY = 1 };
+
+/* Packed parameters of one BEAM MoE block (moe.py:169-192, beam.py:33-48).
+ * Shapes use E = num_experts + num_shared, d_pad = round_up(d_h, 8),
+ * f_pad = round_up(d_ff, 16).  Padding entries are zero.
+ *   norm_w  f32 [d_h]                 (NULL when has_norm == 0)
+ *   gate_wT f32 [2N, d_pad]           rows 0..N-1 = router_w^T, rows N..2N-1 = mask_w^T
+ *   w_gu    wdtype [E, 2*f_pad, d_pad] gate/up rows interleaved in 32-row groups:
+ *           packed row 32*b + i (i<16) = gate feature 16*b+i, 32*b+16+i = up feature 16*b+i
+ *   w_down  wdtype [E, d_pad, f_pad]  (= w_down^T per expert: row = output channel)
+ * Experts 0..N-1 are routed, N..E-1 are the shared experts (weight 1.0, added
+ * after the routed ones, beam.py:163-164). */
+typedef struct {
+  int d_h, d_ff, num_experts, top_k, num_shared;
+  int has_norm;
+  int activation;       /* BEAM_ACT_* */
+  int wdtype;           /* BEAM_BF16 or BEAM_F32 (expert weights and expert inputs) */
+  float mask_threshold; /* keep slot iff pre-activation a >= threshold (0.0f <=> tau = 0.5) */
+  const float* norm_w;
+  const float* gate_wT;
+  const void* w_gu;
+  const void* w_down;
+} beam_layer_t;
+
+/* Optional outputs of beam_layer_forward (any may be NULL except `out`). */
+typedef struct {
+  void* out;               /* [T, d_h], dtype of h: h + y                        */
+  int64_t* topk_ids;       /* [T, K] rank order (RouterDecision.topk_indices)    */
+  float* logits;           /* [T, N] router logits (RouterDecision.logits)       */
+  float* weights;          /* [T, N] dense top-K softmax (RouterDecision.weights)*/
+  float* pre_activation;   /* [T, N] mask router a (MaskDecision.pre_activation) */
+  float* raw_mask;         /* [T, N] sigmoid(a)    (MaskDecision.raw_mask)       */
+  float* mask;             /* [T, N] 1.0 iff a >= threshold (MaskDecision.mask)  */
+  int64_t* masked_ids;     /* [T, K] dispatch.mask_route output                  */
+} beam_outputs_t;
+
+/* Bytes of scratch the entries below need for T tokens, routed-id rows of width
+ * K (0 = the layer's top_k + num_shared) and the given block size. */
+size_t beam_workspace_bytes(const beam_layer_t* layer, int T, int K, int block_size);
+
+/* beam.beam_block_forward(h, block, training=False, block_size) (beam.py:127-165).
+ * h: [T, d_h] of h_dtype (BEAM_F32 or BEAM_BF16). */
+int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, int T,
+                       int block_size, const beam_outputs_t* outputs, void* workspace,
+                       size_t workspace_bytes, beam_stream_t stream);
+
+/* The gating half alone (rms_norm -> topk_route -> mask_forward -> mask_route):
+ * fills the decision outputs of `outputs` (outputs->out is ignored). */
+int beam_gate(const beam_layer_t* layer, const void* h, int h_dtype, int T,
+              const beam_outputs_t* outputs, void* workspace, size_t workspace_bytes,
+              beam_stream_t stream);
+
+/* Dispatch half for externally routed tokens (expert-parallel ranks):
+ * y[t] = sum over k (ascending expert id) of w[t,k] * E_{ids[t,k]}(x[t])  (ids < 0 skipped).
+ * x: [T, d_h] of x_dtype; ids int32 [T, K]; w f32 [T, K]; y f32 [T, d_h]. */
+int beam_moe_execute(const beam_layer_t* layer, const void* x, int x_dtype, int T, int K,
+                     const int32_t* ids, const float* w, float* y, void* workspace,
+                     size_t workspace_bytes, beam_stream_t stream);
+
+/* dispatch.mask_route (_kernels.pyx:17-34): out[t,k] = ids[t,k] if
+ * 0 <= ids[t,k] < N and a[t, ids[t,k]] >= 0 else -1.  a: [T, N] of a_dtype
+ * (BEAM_F32 or BEAM_F64), NaN -> -1. */
+int beam_mask_route(const int64_t* topk_ids, const void* a, int a_dtype, int T, int K, int N,
+                    int64_t* out, beam_stream_t stream);
+
+/* dispatch.align_block (group_by_expert _kernels.pyx:37-66 + padding, __init__.py:106-119).
+ * ids int64 [T, K] (entries outside [0, N) are ignored).  Outputs (int32):
+ *   counts [N]; offsets [N+1] padded exclusive scan (offsets[N] = padded total);
+ *   tokens/slots [cap] with cap = T*K + N*(block_size-1): per expert, the real
+ *   (token, slot) pairs in ascending flat order then -1 padding;
+ *   active [N] ascending ids of experts with counts > 0; meta [4] =
+ *   {num_active, padded_total, real_total, 0}. */
+int beam_group_by_expert(const int64_t* ids, int T, int K, int N, int block_size,
+                         int32_t* counts, int32_t* offsets, int32_t* tokens, int32_t* slots,
+                         int32_t* active, int32_t* meta, beam_stream_t stream);
+
+/* dispatch.grouped_execute (__init__.py:129-157) on a plan from beam_group_by_expert.
+ * x: [T, d_h] of x_dtype, weights_hat f32 [T, N] dense, y f32 [T, d_h].
+ * flags int32[2] (may be NULL): flags[0] = nnz(weights_hat) - real_total,
+ * flags[1] = 1 if a planned slot has zero weight (the reference's ContractErrors). */
+int beam_grouped_execute(const beam_layer_t* layer, const void* x, int x_dtype, int T, int K,
+                         int block_size, const int32_t* counts, const int32_t* offsets,
+                         const int32_t* tokens, const int32_t* slots, const int32_t* active,
+                         const int32_t* meta, const float* weights_hat, float* y, int32_t* flags,
+                         void* workspace, size_t workspace_bytes, beam_stream_t stream);
+
+/* tensor.rms_norm / MoEBlock.normalize (tensor.py:485-508, moe.py:214-215):
+ * out[t] = h[t] * (mean(h[t]^2) + 1e-6)^-1/2 * norm_w, fp32 out [T, d]. */
+int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w, float* out,
+                  beam_stream_t stream);
+
+/* Diagnostics. */
+const char* beam_last_cuda_error(void);
+const char* beam_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BEAM_B200_H */

@@ -1,0 +1,27 @@
+"""B200-native BEAM (Binary Expert Activation Masking) MoE-layer hot path.
+
+A drop-in for the inference path of the reference package ``beamoe``
+(arxiv 2605.14438): same public names as ``beamoe.moe`` / ``beamoe.beam`` /
+``beamoe.dispatch``, computed by hand-written sm_100a CUDA kernels behind the
+C ABI in ``include/beam_b200.h``.  No CPU fallback: without the built library
+or a CUDA device every compute entry raises ``BeamNativeError``.
+"""
+
+from . import dispatch  # noqa: F401
+from ._lib import BeamNativeError  # noqa: F401
+from .beam import MaskDecision, MaskRouter, beam_block_forward, mask_forward, rms_norm  # noqa: F401
+from .moe import (  # noqa: F401
+    Expert,
+    MoEBlock,
+    MoEBlockConfig,
+    RouterDecision,
+    topk_route,
+    topk_select,
+)
+from .tensor import ContractError, NumericError, ShapeError  # noqa: F401
+
+__all__ = [
+    "BeamNativeError", "ContractError", "Expert", "MaskDecision", "MaskRouter", "MoEBlock",
+    "MoEBlockConfig", "NumericError", "RouterDecision", "ShapeError", "beam_block_forward",
+    "dispatch", "mask_forward", "rms_norm", "topk_route", "topk_select",
+]

@@ -1,0 +1,133 @@
+"""ctypes binding of the C ABI in ``include/beam_b200.h`` (``_lib/libbeam_b200.so``).
+
+There is deliberately no fallback: if the library is missing or no CUDA device
+is visible, every entry point raises ``BeamNativeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .tensor import ContractError, ShapeError
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libbeam_b200.so")
+
+BEAM_OK = 0
+BEAM_ERR_ARG = -1
+BEAM_ERR_UNSUPPORTED = -2
+BEAM_ERR_CUDA = -3
+BEAM_ERR_WORKSPACE = -4
+
+BEAM_F32, BEAM_BF16, BEAM_F64 = 0, 1, 2
+BEAM_ACT_SILU, BEAM_ACT_IDENTITY = 0, 1
+
+# every symbol include/beam_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "beam_workspace_bytes",
+    "beam_layer_forward",
+    "beam_gate",
+    "beam_moe_execute",
+    "beam_mask_route",
+    "beam_group_by_expert",
+    "beam_grouped_execute",
+    "beam_rms_norm",
+    "beam_last_cuda_error",
+    "beam_build_info",
+)
+
+
+class BeamNativeError(RuntimeError):
+    """The CUDA library is unavailable or a kernel launch failed."""
+
+
+class LayerDesc(ctypes.Structure):
+    """beam_layer_t."""
+
+    _fields_ = [
+        ("d_h", ctypes.c_int),
+        ("d_ff", ctypes.c_int),
+        ("num_experts", ctypes.c_int),
+        ("top_k", ctypes.c_int),
+        ("num_shared", ctypes.c_int),
+        ("has_norm", ctypes.c_int),
+        ("activation", ctypes.c_int),
+        ("wdtype", ctypes.c_int),
+        ("mask_threshold", ctypes.c_float),
+        ("norm_w", ctypes.c_void_p),
+        ("gate_wT", ctypes.c_void_p),
+        ("w_gu", ctypes.c_void_p),
+        ("w_down", ctypes.c_void_p),
+    ]
+
+
+class Outputs(ctypes.Structure):
+    """beam_outputs_t."""
+
+    _fields_ = [
+        ("out", ctypes.c_void_p),
+        ("topk_ids", ctypes.c_void_p),
+        ("logits", ctypes.c_void_p),
+        ("weights", ctypes.c_void_p),
+        ("pre_activation", ctypes.c_void_p),
+        ("raw_mask", ctypes.c_void_p),
+        ("mask", ctypes.c_void_p),
+        ("masked_ids", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load (once) and type the library."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise BeamNativeError(
+            f"CUDA library not built: {path} missing (run `python -m paper_2605_14438_b200._build`)")
+    lib = ctypes.CDLL(path)
+    P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    LP, OP = ctypes.POINTER(LayerDesc), ctypes.POINTER(Outputs)
+    sig = {
+        "beam_workspace_bytes": (S, [LP, I, I, I]),
+        "beam_layer_forward": (I, [LP, P, I, I, I, OP, P, S, P]),
+        "beam_gate": (I, [LP, P, I, I, OP, P, S, P]),
+        "beam_moe_execute": (I, [LP, P, I, I, I, P, P, P, P, S, P]),
+        "beam_mask_route": (I, [P, P, I, I, I, I, P, P]),
+        "beam_group_by_expert": (I, [P, I, I, I, I, P, P, P, P, P, P, P]),
+        "beam_grouped_execute": (I, [LP, P, I, I, I, I, P, P, P, P, P, P, P, P, P, P, S, P]),
+        "beam_rms_norm": (I, [P, I, I, I, P, P, P]),
+        "beam_last_cuda_error": (ctypes.c_char_p, []),
+        "beam_build_info": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == BEAM_OK:
+        return
+    lib = load()
+    if rc == BEAM_ERR_ARG:
+        raise ContractError(f"{what}: invalid argument")
+    if rc == BEAM_ERR_UNSUPPORTED:
+        raise ShapeError(f"{what}: shape not supported by the sm_100a kernels")
+    if rc == BEAM_ERR_WORKSPACE:
+        raise BeamNativeError(f"{what}: workspace too small")
+    raise BeamNativeError(f"{what}: CUDA error: {lib.beam_last_cuda_error().decode()}")
+
+
+def require_device(t) -> None:
+    import torch
+
+    if not torch.cuda.is_available():
+        raise BeamNativeError("no CUDA device visible: the BEAM B200 kernels have no CPU fallback")
+    if not t.is_cuda:
+        raise BeamNativeError("expected a CUDA tensor")

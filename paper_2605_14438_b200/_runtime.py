@@ -1,0 +1,33 @@
+"""Device plumbing: current stream handle and cached workspaces (torch memory)."""
+
+from __future__ import annotations
+
+import threading
+
+import torch
+
+_lock = threading.Lock()
+_workspaces: dict = {}
+
+
+def stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    """A uint8 scratch buffer of at least ``nbytes`` for the current stream of
+    ``device`` (grown geometrically, reused across calls on that stream)."""
+    key = (device.index if device.index is not None else torch.cuda.current_device(),
+           torch.cuda.current_stream(device).cuda_stream)
+    with _lock:
+        buf = _workspaces.get(key)
+        if buf is None or buf.numel() < nbytes:
+            size = max(nbytes, int(buf.numel() * 1.5) if buf is not None else 0, 1 << 20)
+            buf = torch.empty(size, dtype=torch.uint8, device=device)
+            _workspaces[key] = buf
+        return buf
+
+
+def release_workspaces() -> None:
+    with _lock:
+        _workspaces.clear()

@@ -1,0 +1,197 @@
+"""Binary expert-activation masking: the BEAM layer forward on B200.
+
+Mirrors /root/reference/pkg/src/beamoe/beam.py: ``MaskRouter`` (:33-48),
+``MaskDecision`` (:51-65), ``mask_forward`` (:68-72) and
+``beam_block_forward`` (:127-165).  The whole layer runs as one C-ABI call,
+``beam_layer_forward`` (include/beam_b200.h), i.e. the sm_100a kernel chain
+gating -> masked permute -> grouped SwiGLU experts -> weighted combine.
+
+Threshold rule: one fp32 predicate ``a >= 0`` decides both the
+mask bit and whether the routed id survives (tau = 0.5).  The reference ties
+the ids to ``a >= 0`` (dispatch.mask_route) but the mask to ``sigmoid(a) >= tau``;
+for tau != 0.5 the two disagree and its grouped_execute raises ContractError
+(dispatch/__init__.py:143-144), so ``beam_block_forward`` rejects tau != 0.5 up
+front.  ``mask_forward`` alone honours any tau via a >= logit(tau).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, _runtime
+from .moe import MoEBlock, RouterDecision, _default_device, _gate_call
+from .tensor import ContractError, ShapeError, as_torch
+
+
+@dataclass
+class MaskRouter:
+    """beam.py:33-48: linear mask scorer W_m [d_h, N] (fp32 on the GPU);
+    zero-init opens every mask (a = 0 >= 0)."""
+
+    weight: torch.Tensor
+    tau: float = 0.5
+
+    def __post_init__(self):
+        if not 0.0 < self.tau < 1.0:
+            raise ContractError("tau must lie in (0, 1)")
+        self.weight = as_torch(self.weight)
+
+    @classmethod
+    def zero_init(cls, d_h: int, num_experts: int, tau: float = 0.5, device=None) -> "MaskRouter":
+        dev = torch.device(device) if device is not None else _default_device()
+        return cls(torch.zeros(d_h, num_experts, dtype=torch.float32, device=dev), tau)
+
+
+@dataclass
+class MaskDecision:
+    """beam.py:51-65: pre_activation a, raw_mask sigmoid(a), mask in {0., 1.}."""
+
+    pre_activation: torch.Tensor
+    raw_mask: torch.Tensor
+    mask: torch.Tensor
+
+    @property
+    def binary_mask(self) -> torch.Tensor:
+        return self.mask.to(torch.int64)
+
+
+def _threshold(tau: float) -> float:
+    """a >= logit(tau)  <=>  sigmoid(a) >= tau (exactly 0.0 for tau = 0.5)."""
+    return 0.0 if tau == 0.5 else float(np.float32(math.log(tau / (1.0 - tau))))
+
+
+def mask_forward(x, router: MaskRouter) -> MaskDecision:
+    """beam.py:68-72 on the GPU: a = x W_m (fp32), raw = sigmoid(a), m = a >= logit(tau)."""
+    w = as_torch(router.weight)
+    o = _gate_call(x, None, w, 1, mask_threshold=_threshold(router.tau),
+                   want=("pre_activation", "raw_mask", "mask"))
+    return MaskDecision(pre_activation=o["pre_activation"], raw_mask=o["raw_mask"], mask=o["mask"])
+
+
+def rms_norm(h, weight, eps: float = 1e-6) -> torch.Tensor:
+    """tensor.py:485-508 forward on the GPU (fp32 output)."""
+    if eps != 1e-6:
+        raise ContractError("the sm_100a kernel implements the reference eps = 1e-6")
+    x = as_torch(h)
+    dev = x.device if x.is_cuda else _default_device()
+    x = x.to(dev)
+    if x.dtype not in (torch.float32, torch.bfloat16):
+        x = x.to(torch.float32)
+    x = x.contiguous()
+    w = as_torch(weight).to(dev, torch.float32).contiguous()
+    t, d = x.shape
+    out = torch.empty(t, d, dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.beam_rms_norm(x.data_ptr(), _lib.BEAM_BF16 if x.dtype == torch.bfloat16 else _lib.BEAM_F32,
+                                 t, d, w.data_ptr(), out.data_ptr(), _runtime.stream_handle(dev)),
+               "beam_rms_norm")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# layer forward
+# ---------------------------------------------------------------------------
+
+
+class LayerOutputs:
+    """All outputs of one layer call carved from ONE flat buffer, so a host
+    caller pays a single device->host copy."""
+
+    def __init__(self, t: int, d: int, n: int, k: int, out_dtype: torch.dtype, device, pin=False):
+        es = torch.empty(0, dtype=out_dtype).element_size()
+        spec = [("out", (t, d), out_dtype, es), ("topk_ids", (t, k), torch.int64, 8),
+                ("masked_ids", (t, k), torch.int64, 8)]
+        spec += [(name, (t, n), torch.float32, 4)
+                 for name in ("logits", "weights", "pre_activation", "raw_mask", "mask")]
+        offs, off = [], 0
+        for name, shape, dt, size in spec:
+            off = (off + 255) // 256 * 256
+            offs.append(off)
+            off += int(np.prod(shape)) * size
+        self.nbytes = off
+        kw = dict(dtype=torch.uint8, device=device)
+        self.buf = torch.empty(off, pin_memory=pin, **kw) if pin else torch.empty(off, **kw)
+        self.views = {}
+        for (name, shape, dt, size), o in zip(spec, offs):
+            n_el = int(np.prod(shape))
+            self.views[name] = self.buf[o : o + n_el * size].view(dt).view(shape)
+
+    def __getitem__(self, name):
+        return self.views[name]
+
+    def ctypes_outputs(self) -> _lib.Outputs:
+        o = _lib.Outputs()
+        for name, v in self.views.items():
+            setattr(o, name, v.data_ptr())
+        return o
+
+    def copy_from(self, other: "LayerOutputs") -> None:
+        self.buf.copy_(other.buf, non_blocking=True)
+
+
+def _check_block(block: MoEBlock):
+    if block.mask_router is None:
+        raise ContractError("block has no mask router (attach beam.MaskRouter)")
+    if block.mask_router.tau != 0.5:
+        raise ContractError(
+            "beam_block_forward: mask_route keeps ids with a >= 0 (tau = 0.5) while the mask uses "
+            f"sigmoid(a) >= tau = {block.mask_router.tau}; the reference rejects the mismatch "
+            "(dispatch/__init__.py:143-144)")
+
+
+def layer_forward_into(x: torch.Tensor, block: MoEBlock, outs: LayerOutputs,
+                       block_size: int = 16) -> None:
+    """Launch the fused layer on ``x`` (device, [T, d], bf16/f32) writing into
+    preallocated ``outs`` — no allocation, no sync (CUDA-graph capturable)."""
+    t = x.shape[0]
+    desc = block.layer_desc(0.0)
+    lib = _lib.load()
+    ws_bytes = lib.beam_workspace_bytes(ctypes.byref(desc), t, 0, block_size)
+    ws = _runtime.workspace(ws_bytes, x.device)
+    o = outs.ctypes_outputs()
+    _lib.check(lib.beam_layer_forward(ctypes.byref(desc), x.data_ptr(),
+                                      _lib.BEAM_BF16 if x.dtype == torch.bfloat16 else _lib.BEAM_F32,
+                                      t, block_size, ctypes.byref(o), ws.data_ptr(), ws.numel(),
+                                      _runtime.stream_handle(x.device)),
+               "beam_layer_forward")
+
+
+def beam_block_forward(h, block: MoEBlock, training: bool = True, block_size: int = 16):
+    """beam.py:127-165 -> (h', RouterDecision, MaskDecision).
+
+    ``h`` is [T, d_h] (torch tensor on the GPU or host, numpy array, or a
+    reference ``Tensor``); bf16 and fp32 are computed as given, fp64 as fp32.
+    Host input => host outputs (one H2D copy in, one D2H copy out).
+    ``training=True`` returns the same forward values (the reference pins
+    training == inference to 1e-9, test_beam.py:281-292); there is no autograd
+    tape on this path (training is out of scope)."""
+    _check_block(block)
+    if block_size < 1:
+        raise ContractError("block_size must be >= 1")
+    x = as_torch(h)
+    if x.ndim != 2 or x.shape[1] != block.cfg.d_h:
+        raise ShapeError("h must be [tokens, d_h]")
+    if x.dtype not in (torch.float32, torch.bfloat16):
+        x = x.to(torch.float32)
+    host = not x.is_cuda
+    dev = block.device
+    xd = x.to(dev, non_blocking=True).contiguous() if host else x.contiguous()
+    cfg = block.cfg
+    t = xd.shape[0]
+    outs = LayerOutputs(t, cfg.d_h, cfg.num_experts, cfg.top_k, xd.dtype, dev)
+    if t > 0:
+        layer_forward_into(xd, block, outs, block_size)
+    if host:
+        hb = LayerOutputs(t, cfg.d_h, cfg.num_experts, cfg.top_k, xd.dtype, "cpu",
+                          pin=torch.cuda.is_available())
+        hb.copy_from(outs)
+        torch.cuda.current_stream(dev).synchronize()
+        outs = hb
+    dec = RouterDecision(logits=outs["logits"], topk_indices=outs["topk_ids"], weights=outs["weights"])
+    md = MaskDecision(pre_activation=outs["pre_activation"], raw_mask=outs["raw_mask"], mask=outs["mask"])
+    return outs["out"], dec, md

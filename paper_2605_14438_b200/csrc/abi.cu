@@ -1,0 +1,268 @@
+// C ABI entry points (include/beam_b200.h): argument validation, workspace
+// carving and the launch sequence of each reference-facing operation.
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "beam_common.cuh"
+#include "beam_internal.h"
+
+namespace beam {
+
+static thread_local char g_last_error[256] = "";
+
+cudaError_t record(cudaError_t e) {
+  if (e != cudaSuccess) snprintf(g_last_error, sizeof(g_last_error), "%s", cudaGetErrorString(e));
+  return e;
+}
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
+// Bump allocator over the caller's workspace (256-byte aligned pieces).
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <typename T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+struct LayerWs {
+  float* xn32;
+  void* xact;
+  float* logits2;
+  int32_t* ids32;
+  float* gw;
+  PlanDev plan;
+  float* act;
+  float* opair;
+};
+
+static size_t wbytes(int wdtype) { return wdtype == BEAM_BF16 ? 2 : 4; }
+
+// One layout serves every entry (sized for the largest user, beam_layer_forward).
+static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, LayerWs* o) {
+  const Dims g = dims_of(L);
+  const int Krow = Kids > g.Keff ? Kids : g.Keff;
+  const size_t M = (size_t)T * Krow;
+  const size_t cap = M + (size_t)g.E * (size_t)(bs > 0 ? bs - 1 : 0);
+  Carver c(ws);
+  LayerWs w;
+  w.xn32 = c.take<float>((size_t)T * g.d_pad);
+  w.xact = c.take<char>((size_t)T * g.d_pad * wbytes(L.wdtype));
+  w.logits2 = c.take<float>((size_t)T * 2 * g.N);
+  w.ids32 = c.take<int32_t>(M);
+  w.gw = c.take<float>(M);
+  w.plan.counts = c.take<int32_t>(g.E);
+  w.plan.offsets = c.take<int32_t>(g.E + 1);
+  w.plan.active = c.take<int32_t>(g.E);
+  w.plan.meta = c.take<int32_t>(4);
+  w.plan.tok = c.take<int32_t>(cap);
+  w.plan.slot = c.take<int32_t>(cap);
+  w.plan.w = c.take<float>(cap);
+  w.plan.slot_pos = c.take<int32_t>(M);
+  w.plan.slot_expert = c.take<int32_t>(M);
+  w.act = c.take<float>(cap * g.f_pad);
+  w.opair = c.take<float>(cap * g.d_pad);
+  if (o) *o = w;
+  return c.off + 256;
+}
+
+static int validate(const beam_layer_t* L) {
+  if (!L) return BEAM_ERR_ARG;
+  if (L->d_h < 1 || L->d_ff < 1 || L->num_experts < 1 || L->top_k < 1 ||
+      L->top_k > L->num_experts || L->num_shared < 0)
+    return BEAM_ERR_ARG;
+  if (L->wdtype != BEAM_BF16 && L->wdtype != BEAM_F32) return BEAM_ERR_ARG;
+  if (L->activation != BEAM_ACT_SILU && L->activation != BEAM_ACT_IDENTITY) return BEAM_ERR_ARG;
+  if (L->num_experts > 512 || L->num_experts + L->num_shared > 1024) return BEAM_ERR_UNSUPPORTED;
+  if (!L->gate_wT || !L->w_gu || !L->w_down) return BEAM_ERR_ARG;
+  if (L->has_norm && !L->norm_w) return BEAM_ERR_ARG;
+  return BEAM_OK;
+}
+
+static int status(cudaError_t e) { return record(e) == cudaSuccess ? BEAM_OK : BEAM_ERR_CUDA; }
+
+#define BEAM_TRY(expr)                          \
+  do {                                          \
+    cudaError_t _e = (expr);                    \
+    if (_e != cudaSuccess) return status(_e);   \
+  } while (0)
+
+}  // namespace beam
+
+using namespace beam;
+
+extern "C" {
+
+size_t beam_workspace_bytes(const beam_layer_t* layer, int T, int K, int block_size) {
+  if (validate(layer) != BEAM_OK || T < 0 || K < 0) return 0;
+  return carve(*layer, T, K, block_size < 1 ? 1 : block_size, nullptr, nullptr);
+}
+
+int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, int T,
+                       int block_size, const beam_outputs_t* o, void* workspace,
+                       size_t workspace_bytes, beam_stream_t stream) {
+  int rc = validate(layer);
+  if (rc) return rc;
+  if (T < 0 || block_size < 1 || !o || !o->out || (T > 0 && !h)) return BEAM_ERR_ARG;
+  if (h_dtype != BEAM_F32 && h_dtype != BEAM_BF16) return BEAM_ERR_ARG;
+  if (T == 0) return BEAM_OK;
+  const beam_layer_t& L = *layer;
+  const Dims g = dims_of(L);
+  LayerWs w;
+  if (carve(L, T, 0, block_size, workspace, &w) > workspace_bytes || !workspace)
+    return BEAM_ERR_WORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+
+  BEAM_TRY(launch_norm_pack(h, h_dtype, T, g.d, g.d_pad, L.has_norm ? L.norm_w : nullptr, w.xn32,
+                            w.xact, L.wdtype, s));
+  BEAM_TRY(launch_router_gemm(w.xn32, L.gate_wT, T, 2 * g.N, g.d_pad, w.logits2, s));
+  BEAM_TRY(launch_topk_mask(w.logits2, T, g.N, g.K, g.S, L.mask_threshold, w.ids32, w.gw,
+                            o->topk_ids, o->masked_ids, o->logits, o->weights, o->pre_activation,
+                            o->raw_mask, o->mask, s));
+  BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, T, g.Keff, g.E, block_size, w.plan, s));
+  BEAM_TRY(launch_experts_simt(L, g, w.xact, w.plan, w.act, w.opair, s));
+  BEAM_TRY(launch_combine(w.plan, w.opair, T, g.Keff, g.d, g.d_pad, h, h_dtype, o->out, h_dtype, s));
+  return BEAM_OK;
+}
+
+int beam_gate(const beam_layer_t* layer, const void* h, int h_dtype, int T,
+              const beam_outputs_t* o, void* workspace, size_t workspace_bytes,
+              beam_stream_t stream) {
+  int rc = validate(layer);
+  if (rc) return rc;
+  if (T < 0 || !o || (T > 0 && !h)) return BEAM_ERR_ARG;
+  if (h_dtype != BEAM_F32 && h_dtype != BEAM_BF16) return BEAM_ERR_ARG;
+  if (T == 0) return BEAM_OK;
+  const beam_layer_t& L = *layer;
+  const Dims g = dims_of(L);
+  LayerWs w;
+  if (carve(L, T, 0, 1, workspace, &w) > workspace_bytes || !workspace) return BEAM_ERR_WORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  BEAM_TRY(launch_norm_pack(h, h_dtype, T, g.d, g.d_pad, L.has_norm ? L.norm_w : nullptr, w.xn32,
+                            nullptr, L.wdtype, s));
+  BEAM_TRY(launch_router_gemm(w.xn32, L.gate_wT, T, 2 * g.N, g.d_pad, w.logits2, s));
+  BEAM_TRY(launch_topk_mask(w.logits2, T, g.N, g.K, g.S, L.mask_threshold, w.ids32, w.gw,
+                            o->topk_ids, o->masked_ids, o->logits, o->weights, o->pre_activation,
+                            o->raw_mask, o->mask, s));
+  return BEAM_OK;
+}
+
+int beam_moe_execute(const beam_layer_t* layer, const void* x, int x_dtype, int T, int K,
+                     const int32_t* ids, const float* wts, float* y, void* workspace,
+                     size_t workspace_bytes, beam_stream_t stream) {
+  int rc = validate(layer);
+  if (rc) return rc;
+  if (T < 0 || K < 1 || (T > 0 && (!x || !ids || !wts || !y))) return BEAM_ERR_ARG;
+  if (x_dtype != BEAM_F32 && x_dtype != BEAM_BF16) return BEAM_ERR_ARG;
+  if (T == 0) return BEAM_OK;
+  const beam_layer_t& L = *layer;
+  const Dims g = dims_of(L);
+  LayerWs w;
+  if (carve(L, T, K, 1, workspace, &w) > workspace_bytes || !workspace) return BEAM_ERR_WORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  BEAM_TRY(launch_norm_pack(x, x_dtype, T, g.d, g.d_pad, nullptr, nullptr, w.xact, L.wdtype, s));
+  BEAM_TRY(launch_permute<int32_t>(ids, wts, T, K, g.E, 1, w.plan, s));
+  BEAM_TRY(launch_experts_simt(L, g, w.xact, w.plan, w.act, w.opair, s));
+  BEAM_TRY(launch_combine(w.plan, w.opair, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
+  return BEAM_OK;
+}
+
+int beam_mask_route(const int64_t* topk_ids, const void* a, int a_dtype, int T, int K, int N,
+                    int64_t* out, beam_stream_t stream) {
+  if (T < 0 || K < 0 || N < 1) return BEAM_ERR_ARG;
+  if ((size_t)T * K == 0) return BEAM_OK;
+  if (!topk_ids || !a || !out) return BEAM_ERR_ARG;
+  if (a_dtype != BEAM_F32 && a_dtype != BEAM_F64) return BEAM_ERR_ARG;
+  return status(launch_mask_route(topk_ids, a, a_dtype, T, K, N, out,
+                                  reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int beam_group_by_expert(const int64_t* ids, int T, int K, int N, int block_size,
+                         int32_t* counts, int32_t* offsets, int32_t* tokens, int32_t* slots,
+                         int32_t* active, int32_t* meta, beam_stream_t stream) {
+  if (T < 0 || K < 0 || N < 0 || block_size < 1) return BEAM_ERR_ARG;
+  if (N > 1024) return BEAM_ERR_UNSUPPORTED;
+  if (!offsets || !meta || (N > 0 && (!counts || !active))) return BEAM_ERR_ARG;
+  if ((size_t)T * K > 0 && (!ids || !tokens || !slots)) return BEAM_ERR_ARG;
+  PlanDev p{};
+  p.counts = counts;
+  p.offsets = offsets;
+  p.active = active;
+  p.meta = meta;
+  p.tok = tokens;
+  p.slot = slots;
+  return status(launch_permute<int64_t>(ids, nullptr, T, K, N, block_size, p,
+                                        reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int beam_grouped_execute(const beam_layer_t* layer, const void* x, int x_dtype, int T, int K,
+                         int block_size, const int32_t* counts, const int32_t* offsets,
+                         const int32_t* tokens, const int32_t* slots, const int32_t* active,
+                         const int32_t* meta, const float* weights_hat, float* y, int32_t* flags,
+                         void* workspace, size_t workspace_bytes, beam_stream_t stream) {
+  int rc = validate(layer);
+  if (rc) return rc;
+  if (T < 0 || K < 1 || block_size < 1) return BEAM_ERR_ARG;
+  if (x_dtype != BEAM_F32 && x_dtype != BEAM_BF16) return BEAM_ERR_ARG;
+  if (T == 0) return BEAM_OK;
+  if (!x || !counts || !offsets || !tokens || !slots || !active || !meta || !weights_hat || !y)
+    return BEAM_ERR_ARG;
+  const beam_layer_t& L = *layer;
+  const Dims g = dims_of(L);
+  LayerWs w;
+  if (carve(L, T, K, block_size, workspace, &w) > workspace_bytes || !workspace)
+    return BEAM_ERR_WORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  PlanDev p = w.plan;
+  p.counts = const_cast<int32_t*>(counts);
+  p.offsets = const_cast<int32_t*>(offsets);
+  p.active = const_cast<int32_t*>(active);
+  p.meta = const_cast<int32_t*>(meta);
+  p.tok = const_cast<int32_t*>(tokens);
+  p.slot = const_cast<int32_t*>(slots);
+  BEAM_TRY(launch_norm_pack(x, x_dtype, T, g.d, g.d_pad, nullptr, nullptr, w.xact, L.wdtype, s));
+  BEAM_TRY(launch_plan_prepare(counts, offsets, tokens, slots, meta, weights_hat, T, K, g.N, p,
+                               flags, s));
+  BEAM_TRY(launch_experts_simt(L, g, w.xact, p, w.act, w.opair, s));
+  BEAM_TRY(launch_combine(p, w.opair, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
+  return BEAM_OK;
+}
+
+int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w, float* out,
+                  beam_stream_t stream) {
+  if (T < 0 || d < 1) return BEAM_ERR_ARG;
+  if (T == 0) return BEAM_OK;
+  if (!h || !norm_w || !out) return BEAM_ERR_ARG;
+  if (h_dtype != BEAM_F32 && h_dtype != BEAM_BF16) return BEAM_ERR_ARG;
+  return status(launch_norm_pack(h, h_dtype, T, d, d, norm_w, out, nullptr, BEAM_F32,
+                                 reinterpret_cast<cudaStream_t>(stream)));
+}
+
+const char* beam_last_cuda_error(void) { return g_last_error; }
+
+#define BEAM_STR2(x) #x
+#define BEAM_STR(x) BEAM_STR2(x)
+const char* beam_build_info(void) {
+  return "beam_b200 sm_100a nvcc " BEAM_STR(__CUDACC_VER_MAJOR__) "." BEAM_STR(__CUDACC_VER_MINOR__);
+}
+
+}  // extern "C"

@@ -1,0 +1,78 @@
+// Internal launcher declarations shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/beam_b200.h"
+
+namespace beam {
+
+// Geometry derived from a beam_layer_t.
+struct Dims {
+  int d, f, N, K, S, E, Keff, d_pad, f_pad;
+};
+
+inline Dims dims_of(const beam_layer_t& L) {
+  Dims g;
+  g.d = L.d_h;
+  g.f = L.d_ff;
+  g.N = L.num_experts;
+  g.K = L.top_k;
+  g.S = L.num_shared;
+  g.E = L.num_experts + L.num_shared;
+  g.Keff = L.top_k + L.num_shared;
+  g.d_pad = (L.d_h + 7) / 8 * 8;
+  g.f_pad = (L.d_ff + 15) / 16 * 16;
+  return g;
+}
+
+// Device-side dispatch plan (all int32 unless noted), carved from workspace.
+struct PlanDev {
+  int32_t* counts;       // [E]
+  int32_t* offsets;      // [E+1] padded exclusive scan
+  int32_t* active;       // [E]
+  int32_t* meta;         // [4] num_active, padded_total, real_total, flag
+  int32_t* tok;          // [cap]
+  int32_t* slot;         // [cap]
+  float* w;              // [cap] routing weight of each planned position
+  int32_t* slot_pos;     // [T*Keff] position of (t,k) in the plan, -1 if dropped
+  int32_t* slot_expert;  // [T*Keff] expert of (t,k), -1 if dropped
+};
+
+int num_sms();
+cudaError_t record(cudaError_t e);
+
+// gate.cu
+cudaError_t launch_norm_pack(const void* h, int h_dtype, int T, int d, int d_pad,
+                             const float* norm_w, float* xn32, void* xact, int act_dtype,
+                             cudaStream_t s);
+cudaError_t launch_router_gemm(const float* xn32, const float* gate_wT, int T, int cols,
+                               int d_pad, float* L, cudaStream_t s);
+cudaError_t launch_topk_mask(const float* L, int T, int N, int K, int S, float thr,
+                             int32_t* ids32, float* gw, int64_t* topk_ids, int64_t* masked_ids,
+                             float* logits, float* weights, float* pre_act, float* raw_mask,
+                             float* mask, cudaStream_t s);
+cudaError_t launch_mask_route(const int64_t* ids, const void* a, int a_dtype, int T, int K,
+                              int N, int64_t* out, cudaStream_t s);
+
+// permute.cu
+template <typename IdT>
+cudaError_t launch_permute(const IdT* ids, const float* w, int T, int K, int E, int bs,
+                           const PlanDev& p, cudaStream_t s);
+cudaError_t launch_plan_prepare(const int32_t* counts, const int32_t* offsets,
+                                const int32_t* tokens, const int32_t* slots, const int32_t* meta,
+                                const float* weights_hat, int T, int K, int N,
+                                const PlanDev& p, int32_t* flags, cudaStream_t s);
+
+// experts_simt.cu
+cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, const void* xact,
+                                const PlanDev& p, float* act, float* opair, cudaStream_t s);
+
+// combine.cu
+cudaError_t launch_combine(const PlanDev& p, const float* opair, int T, int Keff, int d, int d_pad,
+                           const void* h, int h_dtype, void* out, int out_dtype,
+                           cudaStream_t s);
+
+}  // namespace beam

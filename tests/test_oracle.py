@@ -8,6 +8,7 @@ import pytest
 
 from oracle import beam_oracle as O
 from oracle import ref
+from _beamtest import golden_block
 
 
 def _plan_flat(plan):
@@ -44,17 +45,6 @@ def test_topk_route_golden(golden):
         assert np.array_equal(dec.topk_indices, g[f"ids_{i}"]), i
         assert np.array_equal(dec.logits, g[f"logits_{i}"]), i
         np.testing.assert_allclose(dec.weights, g[f"weights_{i}"], rtol=0, atol=1e-15)
-
-
-def golden_block(g, i):
-    seed, d, f, n, k, sh, norm, t, bs = (int(v) for v in g[f"c{i}_cfg"])
-    p = f"c{i}_"
-    experts = [(g[p + "w_gate"][e], g[p + "w_up"][e], g[p + "w_down"][e]) for e in range(n)]
-    shared = [(g[p + "s_gate"][s], g[p + "s_up"][s], g[p + "s_down"][s]) for s in range(sh)]
-    block = O.OracleBlock(d_h=d, d_ff=f, num_experts=n, top_k=k, router_w=g[p + "router_w"],
-                          experts=experts, shared=shared, norm_w=np.ones(d) if norm else None,
-                          mask_w=g[p + "mask_w"])
-    return block, g[p + "h"], bs
 
 
 def test_layer_golden(golden):
