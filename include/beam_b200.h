@@ -145,7 +145,15 @@ int beam_grouped_execute(const beam_layer_t* layer, const void* x, int x_dtype, 
 int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w, float* out,
                   beam_stream_t stream);
 
-/* Diagnostics. */
+/* Diagnostics.
+ * beam_kernel_launches: kernels this library launched since load.
+ * beam_profile_begin/end: record CUDA events on the launch stream at the stage
+ * boundaries of the next `max_calls` beam_layer_forward calls; _end syncs on the
+ * last one and returns per-stage sums in ms: stage_ms[5] = {gate, permute,
+ * experts_gateup, experts_down, combine}. */
+unsigned long long beam_kernel_launches(void);
+int beam_profile_begin(int max_calls);
+int beam_profile_end(float* stage_ms, int* calls);
 const char* beam_last_cuda_error(void);
 const char* beam_build_info(void);
 

@@ -33,6 +33,9 @@ EXPORTS = (
     "beam_group_by_expert",
     "beam_grouped_execute",
     "beam_rms_norm",
+    "beam_kernel_launches",
+    "beam_profile_begin",
+    "beam_profile_end",
     "beam_last_cuda_error",
     "beam_build_info",
 )
@@ -100,6 +103,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_group_by_expert": (I, [P, I, I, I, I, P, P, P, P, P, P, P]),
         "beam_grouped_execute": (I, [LP, P, I, I, I, I, P, P, P, P, P, P, P, P, P, P, S, P]),
         "beam_rms_norm": (I, [P, I, I, I, P, P, P]),
+        "beam_kernel_launches": (ctypes.c_ulonglong, []),
+        "beam_profile_begin": (I, [I]),
+        "beam_profile_end": (I, [P, P]),
         "beam_last_cuda_error": (ctypes.c_char_p, []),
         "beam_build_info": (ctypes.c_char_p, []),
     }

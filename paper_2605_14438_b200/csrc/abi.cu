@@ -3,7 +3,8 @@
 #include <stdio.h>
 #include <string.h>
 
-#include <mutex>
+#include <atomic>
+#include <vector>
 
 #include "beam_common.cuh"
 #include "beam_internal.h"
@@ -15,6 +16,24 @@ static thread_local char g_last_error[256] = "";
 cudaError_t record(cudaError_t e) {
   if (e != cudaSuccess) snprintf(g_last_error, sizeof(g_last_error), "%s", cudaGetErrorString(e));
   return e;
+}
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+// Stage timing for beam_layer_forward (diagnostics; see beam_profile_begin).
+constexpr int kStageMarks = 6;  // start, gate, permute, gateup, down, combine
+struct Profiler {
+  bool on = false;
+  int max_calls = 0, calls = 0;
+  std::vector<cudaEvent_t> ev;
+};
+static Profiler g_prof;
+
+static void prof_mark(int mark, cudaStream_t s) {
+  if (!g_prof.on || g_prof.calls >= g_prof.max_calls) return;
+  cudaEventRecord(g_prof.ev[(size_t)g_prof.calls * kStageMarks + mark], s);
+  if (mark == kStageMarks - 1) ++g_prof.calls;
 }
 
 int num_sms() {
@@ -132,15 +151,22 @@ int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, in
     return BEAM_ERR_WORKSPACE;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
 
+  prof_mark(0, s);
   BEAM_TRY(launch_norm_pack(h, h_dtype, T, g.d, g.d_pad, L.has_norm ? L.norm_w : nullptr, w.xn32,
                             w.xact, L.wdtype, s));
   BEAM_TRY(launch_router_gemm(w.xn32, L.gate_wT, T, 2 * g.N, g.d_pad, w.logits2, s));
   BEAM_TRY(launch_topk_mask(w.logits2, T, g.N, g.K, g.S, L.mask_threshold, w.ids32, w.gw,
                             o->topk_ids, o->masked_ids, o->logits, o->weights, o->pre_activation,
                             o->raw_mask, o->mask, s));
+  prof_mark(1, s);
   BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, T, g.Keff, g.E, block_size, w.plan, s));
-  BEAM_TRY(launch_experts_simt(L, g, w.xact, w.plan, w.act, w.opair, s));
+  prof_mark(2, s);
+  BEAM_TRY(launch_gateup_simt(L, g, w.xact, w.plan, w.act, s));
+  prof_mark(3, s);
+  BEAM_TRY(launch_down_simt(L, g, w.plan, w.act, w.opair, s));
+  prof_mark(4, s);
   BEAM_TRY(launch_combine(w.plan, w.opair, T, g.Keff, g.d, g.d_pad, h, h_dtype, o->out, h_dtype, s));
+  prof_mark(5, s);
   return BEAM_OK;
 }
 
@@ -255,6 +281,40 @@ int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w,
   if (h_dtype != BEAM_F32 && h_dtype != BEAM_BF16) return BEAM_ERR_ARG;
   return status(launch_norm_pack(h, h_dtype, T, d, d, norm_w, out, nullptr, BEAM_F32,
                                  reinterpret_cast<cudaStream_t>(stream)));
+}
+
+unsigned long long beam_kernel_launches(void) { return g_launches.load(); }
+
+int beam_profile_begin(int max_calls) {
+  if (max_calls < 1) return BEAM_ERR_ARG;
+  for (cudaEvent_t e : g_prof.ev) cudaEventDestroy(e);
+  g_prof.ev.assign((size_t)max_calls * kStageMarks, nullptr);
+  for (auto& e : g_prof.ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return status(cudaGetLastError());
+  g_prof.max_calls = max_calls;
+  g_prof.calls = 0;
+  g_prof.on = true;
+  return BEAM_OK;
+}
+
+int beam_profile_end(float* stage_ms, int* calls) {
+  if (!g_prof.on) return BEAM_ERR_ARG;
+  g_prof.on = false;
+  for (int k = 0; k < kStageMarks - 1; ++k) stage_ms[k] = 0.0f;
+  if (g_prof.calls > 0) {
+    cudaError_t e = cudaEventSynchronize(g_prof.ev[(size_t)g_prof.calls * kStageMarks - 1]);
+    if (e != cudaSuccess) return status(e);
+  }
+  for (int c = 0; c < g_prof.calls; ++c)
+    for (int k = 0; k < kStageMarks - 1; ++k) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, g_prof.ev[(size_t)c * kStageMarks + k], g_prof.ev[(size_t)c * kStageMarks + k + 1]);
+      stage_ms[k] += ms;
+    }
+  *calls = g_prof.calls;
+  for (cudaEvent_t e : g_prof.ev) cudaEventDestroy(e);
+  g_prof.ev.clear();
+  return BEAM_OK;
 }
 
 const char* beam_last_cuda_error(void) { return g_last_error; }

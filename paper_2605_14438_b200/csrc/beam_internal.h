@@ -43,6 +43,7 @@ struct PlanDev {
 
 int num_sms();
 cudaError_t record(cudaError_t e);
+void count_launches(int n);  // bookkeeping for beam_kernel_launches()
 
 // gate.cu
 cudaError_t launch_norm_pack(const void* h, int h_dtype, int T, int d, int d_pad,
@@ -67,8 +68,16 @@ cudaError_t launch_plan_prepare(const int32_t* counts, const int32_t* offsets,
                                 const PlanDev& p, int32_t* flags, cudaStream_t s);
 
 // experts_simt.cu
-cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, const void* xact,
-                                const PlanDev& p, float* act, float* opair, cudaStream_t s);
+cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void* xact,
+                               const PlanDev& p, float* act, cudaStream_t s);
+cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, const PlanDev& p,
+                             const float* act, float* opair, cudaStream_t s);
+inline cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, const void* xact,
+                                       const PlanDev& p, float* act, float* opair, cudaStream_t s) {
+  cudaError_t e = launch_gateup_simt(L, g, xact, p, act, s);
+  if (e != cudaSuccess) return e;
+  return launch_down_simt(L, g, p, act, opair, s);
+}
 
 // combine.cu
 cudaError_t launch_combine(const PlanDev& p, const float* opair, int T, int Keff, int d, int d_pad,

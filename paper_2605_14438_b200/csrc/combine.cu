@@ -64,6 +64,7 @@ cudaError_t launch_combine(const PlanDev& p, const float* opair, int T, int Keff
     combine_kernel<__nv_bfloat16, float><<<T, 256, smem, s>>>(p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const __nv_bfloat16*)h, (float*)out);
   else
     combine_kernel<float, __nv_bfloat16><<<T, 256, smem, s>>>(p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const float*)h, (__nv_bfloat16*)out);
+  count_launches(1);
   return cudaGetLastError();
 }
 

@@ -183,8 +183,8 @@ __global__ void __launch_bounds__(256, 2) down_kernel(const TW* __restrict__ Wd,
   }
 }
 
-cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, const void* xact,
-                                const PlanDev& p, float* act, float* opair, cudaStream_t s) {
+cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void* xact,
+                               const PlanDev& p, float* act, cudaStream_t s) {
   const int grid = num_sms() * 2;
   if (L.wdtype == BEAM_BF16) {
     using TW = __nv_bfloat16;
@@ -192,15 +192,25 @@ cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, const void
       gateup_kernel<TW, BEAM_ACT_SILU><<<grid, 256, 0, s>>>((const TW*)L.w_gu, (const TW*)xact, g.d_pad, g.f_pad, p, act);
     else
       gateup_kernel<TW, BEAM_ACT_IDENTITY><<<grid, 256, 0, s>>>((const TW*)L.w_gu, (const TW*)xact, g.d_pad, g.f_pad, p, act);
-    down_kernel<TW><<<grid, 256, 0, s>>>((const TW*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
   } else {
     using TW = float;
     if (L.activation == BEAM_ACT_SILU)
       gateup_kernel<TW, BEAM_ACT_SILU><<<grid, 256, 0, s>>>((const TW*)L.w_gu, (const TW*)xact, g.d_pad, g.f_pad, p, act);
     else
       gateup_kernel<TW, BEAM_ACT_IDENTITY><<<grid, 256, 0, s>>>((const TW*)L.w_gu, (const TW*)xact, g.d_pad, g.f_pad, p, act);
-    down_kernel<TW><<<grid, 256, 0, s>>>((const TW*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
   }
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, const PlanDev& p,
+                             const float* act, float* opair, cudaStream_t s) {
+  const int grid = num_sms() * 2;
+  if (L.wdtype == BEAM_BF16)
+    down_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+  else
+    down_kernel<float><<<grid, 256, 0, s>>>((const float*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+  count_launches(1);
   return cudaGetLastError();
 }
 

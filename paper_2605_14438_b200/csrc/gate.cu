@@ -63,6 +63,7 @@ cudaError_t launch_norm_pack(const void* h, int h_dtype, int T, int d, int d_pad
     norm_pack_kernel<__nv_bfloat16, float><<<grid, block, 0, s>>>((const __nv_bfloat16*)h, T, d, d_pad, norm_w, xn32, (float*)xact);
   else
     norm_pack_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, block, 0, s>>>((const __nv_bfloat16*)h, T, d, d_pad, norm_w, xn32, (__nv_bfloat16*)xact);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -148,6 +149,7 @@ cudaError_t launch_router_gemm(const float* xn32, const float* gate_wT, int T, i
     dim3 grid(ceil_div(T, 64), ceil_div(cols, 64));
     router_gemm_kernel<64, 64><<<grid, 256, 0, s>>>(xn32, gate_wT, T, cols, d_pad, L);
   }
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -256,6 +258,7 @@ cudaError_t launch_topk_mask(const float* L, int T, int N, int K, int S, float t
   topk_mask_kernel<<<ceil_div(T, 8), 256, 0, s>>>(L, T, N, K, S, thr, ids32, gw, topk_ids,
                                                   masked_ids, logits, weights, pre_act, raw_mask,
                                                   mask);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -286,6 +289,7 @@ cudaError_t launch_mask_route(const int64_t* ids, const void* a, int a_dtype, in
     mask_route_kernel<double><<<grid, 256, 0, s>>>(ids, (const double*)a, T, K, N, out);
   else
     mask_route_kernel<float><<<grid, 256, 0, s>>>(ids, (const float*)a, T, K, N, out);
+  count_launches(1);
   return cudaGetLastError();
 }
 

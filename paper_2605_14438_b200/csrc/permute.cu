@@ -161,6 +161,7 @@ cudaError_t launch_permute(const IdT* ids, const float* w, int T, int K, int E, 
     attr_set = true;
   }
   permute_kernel<IdT><<<1, kPermuteThreads, smem, s>>>(ids, w, T, K, E, bs, p);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -212,11 +213,15 @@ cudaError_t launch_plan_prepare(const int32_t* counts, const int32_t* offsets,
   if ((e = cudaMemsetAsync(p.slot_pos, 0xff, (size_t)T * K * sizeof(int32_t), s))) return e;
   if ((e = cudaMemsetAsync(p.slot_expert, 0xff, (size_t)T * K * sizeof(int32_t), s))) return e;
   if (flags && (e = cudaMemsetAsync(flags, 0, 2 * sizeof(int32_t), s))) return e;
-  if (N > 0) plan_prepare_kernel<<<N, 256, 0, s>>>(counts, offsets, tokens, slots, weights_hat, T, K, N, p, flags);
+  if (N > 0) {
+    plan_prepare_kernel<<<N, 256, 0, s>>>(counts, offsets, tokens, slots, weights_hat, T, K, N, p, flags);
+    count_launches(1);
+  }
   if (flags) {
     const long long n = (long long)T * N;
     const int grid = (int)std::min<long long>(1024, std::max<long long>(1, (n + 255) / 256));
     nnz_count_kernel<<<grid, 256, 0, s>>>(weights_hat, n, meta, flags);
+    count_launches(1);
   }
   return cudaGetLastError();
 }

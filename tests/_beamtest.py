@@ -72,3 +72,10 @@ def golden_block(g, i):
                           experts=experts, shared=shared, norm_w=np.ones(d) if norm else None,
                           mask_w=g[p + "mask_w"])
     return block, g[p + "h"], bs
+
+
+def mask_margin_ok(ref, tol: float) -> np.ndarray:
+    """Per token: every candidate's mask pre-activation is either exactly 0 (exact
+    in both precisions; inclusive threshold) or farther than tol from it."""
+    a = np.take_along_axis(ref.mask.pre_activation, ref.decision.topk_indices, 1)
+    return np.all((np.abs(a) > tol) | (a == 0.0), axis=1)

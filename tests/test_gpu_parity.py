@@ -18,7 +18,7 @@ if not torch.cuda.is_available():  # the gpu marker is deselected on CPU runs
 import paper_2605_14438_b200 as B  # noqa: E402
 from paper_2605_14438_b200 import dispatch as D  # noqa: E402
 from oracle import beam_oracle as O  # noqa: E402
-from _beamtest import golden_block, matched_blocks, normwise_rel, topk_margin_ok  # noqa: E402
+from _beamtest import golden_block, mask_margin_ok, matched_blocks, normwise_rel, topk_margin_ok  # noqa: E402
 
 TOL_BF16 = 1e-2
 TOL_F32 = 1e-4
@@ -94,7 +94,7 @@ def test_layer_golden(golden, dtype_name, tol):
         ref = O.beam_block_forward(h32, ob, block_size=bs)
         out, dec, md = B.beam_block_forward(torch.from_numpy(h32).float().cuda(), gb, training=False, block_size=bs)
         ok = topk_margin_ok(ref.decision.logits, ob.top_k, 1e-4)
-        ok &= np.all(np.abs(np.take_along_axis(ref.mask.pre_activation, ref.decision.topk_indices, 1)) > 1e-4, axis=1)
+        ok &= mask_margin_ok(ref, 1e-4)
         assert ok.mean() > 0.8
         assert np.array_equal(_np(dec.topk_indices)[ok], ref.decision.topk_indices[ok]), i
         assert np.array_equal(_np(md.mask)[ok], ref.mask.mask[ok]), i
@@ -158,7 +158,7 @@ def test_layer_q30_decode_bf16(t, mask_std):
     ob, gb, h64, ref, out, dec, md = _layer_case(2048, 768, 128, 8, t, 100 + t, mask_std, "bf16",
                                                  h_dtype=torch.bfloat16)
     ok = topk_margin_ok(ref.decision.logits, 8, 1e-5)
-    ok &= np.all(np.abs(np.take_along_axis(ref.mask.pre_activation, ref.decision.topk_indices, 1)) > 1e-5, axis=1)
+    ok &= mask_margin_ok(ref, 1e-5)
     assert np.array_equal(_np(dec.topk_indices)[ok], ref.decision.topk_indices[ok])
     assert np.array_equal(_np(md.mask)[ok], ref.mask.mask[ok])
     o = _np(out.float()).astype(np.float64)
@@ -173,7 +173,7 @@ def test_layer_q30_fp32_input_update():
     """fp32 activations in/out: the MoE update y itself within the bf16 tolerance."""
     ob, gb, h64, ref, out, dec, md = _layer_case(2048, 768, 128, 8, 32, 7, 1 / np.sqrt(2048), "bf16")
     ok = topk_margin_ok(ref.decision.logits, 8, 1e-5)
-    ok &= np.all(np.abs(np.take_along_axis(ref.mask.pre_activation, ref.decision.topk_indices, 1)) > 1e-5, axis=1)
+    ok &= mask_margin_ok(ref, 1e-5)
     y = _np(out).astype(np.float64) - h64
     assert normwise_rel(y[ok], ref.y[ok]) <= TOL_BF16
 
@@ -182,7 +182,7 @@ def test_layer_tiny_fp32():
     """configs[0]: tiny N=8 K=2 d=256 f=512 T=1024, fp32 -> 1e-4."""
     ob, gb, h64, ref, out, dec, md = _layer_case(256, 512, 8, 2, 1024, 3, 1 / 16, "f32")
     ok = topk_margin_ok(ref.decision.logits, 2, 1e-5)
-    ok &= np.all(np.abs(np.take_along_axis(ref.mask.pre_activation, ref.decision.topk_indices, 1)) > 1e-5, axis=1)
+    ok &= mask_margin_ok(ref, 1e-5)
     assert ok.mean() > 0.95
     assert np.array_equal(_np(dec.topk_indices)[ok], ref.decision.topk_indices[ok])
     o = _np(out).astype(np.float64)
