@@ -324,11 +324,16 @@ class MoEBlock:
         key = (self.router_w._version, id(mw), mw._version if mw is not None else -1,
                self.norm_w._version if self.norm_w is not None else -1)
         if key != self._pack_key:
-            gate = torch.zeros(2 * cfg.num_experts, cfg.d_pad, dtype=torch.float32, device=self.device)
+            # repacked in place: captured CUDA graphs keep a valid pointer
+            if getattr(self, "gate_wT", None) is None:
+                self.gate_wT = torch.zeros(2 * cfg.num_experts, cfg.d_pad, dtype=torch.float32,
+                                           device=self.device)
+            gate = self.gate_wT
             gate[: cfg.num_experts, : cfg.d_h] = self.router_w.t()
             if mw is not None:
                 gate[cfg.num_experts :, : cfg.d_h] = mw.t()
-            self.gate_wT = gate
+            else:
+                gate[cfg.num_experts :].zero_()
             self._pack_key = key
         d = _lib.LayerDesc()
         d.d_h, d.d_ff, d.num_experts, d.top_k = cfg.d_h, cfg.d_ff, cfg.num_experts, cfg.top_k
