@@ -152,6 +152,10 @@ int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w,
  * last one and returns per-stage sums in ms: stage_ms[5] = {gate, permute,
  * experts_gateup, experts_down, combine}. */
 unsigned long long beam_kernel_launches(void);
+/* Expert-stage kernel choice for beam_layer_forward: 0 = auto (tcgen05 grouped
+ * GEMM when bf16 weights and >= 32 tokens per expert on average, else the
+ * weight-streaming kernels), 1 = force weight streaming, 2 = force tcgen05. */
+int beam_set_expert_path(int mode);
 int beam_profile_begin(int max_calls);
 int beam_profile_end(float* stage_ms, int* calls);
 const char* beam_last_cuda_error(void);

@@ -9,7 +9,7 @@ or a CUDA device every compute entry raises ``BeamNativeError``.
 
 from . import dispatch  # noqa: F401
 from ._lib import BeamNativeError  # noqa: F401
-from .beam import MaskDecision, MaskRouter, beam_block_forward, mask_forward, rms_norm  # noqa: F401
+from .beam import MaskDecision, MaskRouter, beam_block_forward, mask_forward, rms_norm, set_expert_path  # noqa: F401
 from .moe import (  # noqa: F401
     Expert,
     MoEBlock,

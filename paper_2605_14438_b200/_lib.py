@@ -34,6 +34,7 @@ EXPORTS = (
     "beam_grouped_execute",
     "beam_rms_norm",
     "beam_kernel_launches",
+    "beam_set_expert_path",
     "beam_profile_begin",
     "beam_profile_end",
     "beam_last_cuda_error",
@@ -104,6 +105,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_grouped_execute": (I, [LP, P, I, I, I, I, P, P, P, P, P, P, P, P, P, P, S, P]),
         "beam_rms_norm": (I, [P, I, I, I, P, P, P]),
         "beam_kernel_launches": (ctypes.c_ulonglong, []),
+        "beam_set_expert_path": (I, [I]),
         "beam_profile_begin": (I, [I]),
         "beam_profile_end": (I, [P, P]),
         "beam_last_cuda_error": (ctypes.c_char_p, []),

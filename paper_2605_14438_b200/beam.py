@@ -195,3 +195,11 @@ def beam_block_forward(h, block: MoEBlock, training: bool = True, block_size: in
     dec = RouterDecision(logits=outs["logits"], topk_indices=outs["topk_ids"], weights=outs["weights"])
     md = MaskDecision(pre_activation=outs["pre_activation"], raw_mask=outs["raw_mask"], mask=outs["mask"])
     return outs["out"], dec, md
+
+
+def set_expert_path(mode: str = "auto") -> None:
+    """Choose the expert-stage kernels of beam_block_forward: "auto" (tcgen05
+    grouped GEMM for prefill-sized batches, weight streaming for decode),
+    "simt" (weight streaming always) or "tc" (tcgen05 always, bf16 weights)."""
+    code = {"auto": 0, "simt": 1, "tc": 2}[mode]
+    _lib.check(_lib.load().beam_set_expert_path(code), "beam_set_expert_path")

@@ -63,10 +63,24 @@ struct Carver {
   }
 };
 
+// Expert path choice: 0 = auto, 1 = weight-streaming SIMT, 2 = tcgen05 grouped GEMM.
+static std::atomic<int> g_expert_path{0};
+
+static bool use_tc(const beam_layer_t& L, const Dims& g, int T, int Krow) {
+  const int mode = g_expert_path.load();
+  if (mode == 1 || !tc_supported(L, g)) return false;
+  if (mode == 2) return true;
+  return (long long)T * Krow >= 32LL * g.E;  // >= 32 tokens per expert on average
+}
+
 struct LayerWs {
-  float* xn32;
-  void* xact;
-  float* logits2;
+  bool tc;
+  int cap;
+  void* xperm;     // [cap, d_pad] bf16 x_n in plan order (tc path)
+  void* act16;     // [cap, f_pad] bf16 (tc path)
+  void* xpad;      // [T, d_pad] input rows re-strided (only when d_h % 8 != 0)
+  float* inv;      // [T] inverse RMS per token
+  float* logits2;  // [splits][T][2N] projection partials
   int32_t* ids32;
   float* gw;
   PlanDev plan;
@@ -74,9 +88,8 @@ struct LayerWs {
   float* opair;
 };
 
-static size_t wbytes(int wdtype) { return wdtype == BEAM_BF16 ? 2 : 4; }
-
 // One layout serves every entry (sized for the largest user, beam_layer_forward).
+// x_bytes: element size of the activation rows (4 covers both dtypes).
 static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, LayerWs* o) {
   const Dims g = dims_of(L);
   const int Krow = Kids > g.Keff ? Kids : g.Keff;
@@ -84,9 +97,13 @@ static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, La
   const size_t cap = M + (size_t)g.E * (size_t)(bs > 0 ? bs - 1 : 0);
   Carver c(ws);
   LayerWs w;
-  w.xn32 = c.take<float>((size_t)T * g.d_pad);
-  w.xact = c.take<char>((size_t)T * g.d_pad * wbytes(L.wdtype));
-  w.logits2 = c.take<float>((size_t)T * 2 * g.N);
+  w.tc = use_tc(L, g, T, Krow);
+  w.cap = (int)cap;
+  w.xperm = w.tc ? c.take<__nv_bfloat16>(cap * g.d_pad) : nullptr;
+  w.act16 = w.tc ? c.take<__nv_bfloat16>(cap * g.f_pad) : nullptr;
+  w.xpad = g.d != g.d_pad ? c.take<float>((size_t)T * g.d_pad) : nullptr;
+  w.inv = c.take<float>((size_t)T);
+  w.logits2 = c.take<float>((size_t)router_splits(T, 2 * g.N, g.d_pad) * T * 2 * g.N);
   w.ids32 = c.take<int32_t>(M);
   w.gw = c.take<float>(M);
   w.plan.counts = c.take<int32_t>(g.E);
@@ -98,10 +115,21 @@ static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, La
   w.plan.w = c.take<float>(cap);
   w.plan.slot_pos = c.take<int32_t>(M);
   w.plan.slot_expert = c.take<int32_t>(M);
-  w.act = c.take<float>(cap * g.f_pad);
+  w.act = w.tc ? nullptr : c.take<float>(cap * g.f_pad);
   w.opair = c.take<float>(cap * g.d_pad);
   if (o) *o = w;
   return c.off + 256;
+}
+
+// Input rows with stride d_pad (a padded copy in the workspace when needed).
+static cudaError_t strided_input(const Dims& g, const void* h, int h_dtype, int T, LayerWs& w,
+                                 const void** X, cudaStream_t s) {
+  if (g.d == g.d_pad) {
+    *X = h;
+    return cudaSuccess;
+  }
+  *X = w.xpad;
+  return launch_pad_rows(h, h_dtype, T, g.d, g.d_pad, w.xpad, h_dtype, s);
 }
 
 static int validate(const beam_layer_t* L) {
@@ -136,6 +164,18 @@ size_t beam_workspace_bytes(const beam_layer_t* layer, int T, int K, int block_s
   return carve(*layer, T, K, block_size < 1 ? 1 : block_size, nullptr, nullptr);
 }
 
+// The gating half shared by beam_layer_forward and beam_gate.
+static cudaError_t run_gate(const beam_layer_t& L, const Dims& g, const void* X, int h_dtype, int T,
+                            const beam_outputs_t* o, LayerWs& w, cudaStream_t s) {
+  const float* nw = L.has_norm ? L.norm_w : nullptr;
+  cudaError_t e = launch_router(X, h_dtype, nw, L.gate_wT, T, 2 * g.N, g.d, g.d_pad, w.logits2, s);
+  if (e != cudaSuccess) return e;
+  return launch_topk_mask(w.logits2, router_splits(T, 2 * g.N, g.d_pad), X, h_dtype, g.d, g.d_pad,
+                          L.has_norm, T, g.N, g.K, g.S, L.mask_threshold, w.inv, w.ids32, w.gw,
+                          o->topk_ids, o->masked_ids, o->logits, o->weights, o->pre_activation,
+                          o->raw_mask, o->mask, s);
+}
+
 int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, int T,
                        int block_size, const beam_outputs_t* o, void* workspace,
                        size_t workspace_bytes, beam_stream_t stream) {
@@ -150,21 +190,27 @@ int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, in
   if (carve(L, T, 0, block_size, workspace, &w) > workspace_bytes || !workspace)
     return BEAM_ERR_WORKSPACE;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const void* X = nullptr;
 
   prof_mark(0, s);
-  BEAM_TRY(launch_norm_pack(h, h_dtype, T, g.d, g.d_pad, L.has_norm ? L.norm_w : nullptr, w.xn32,
-                            w.xact, L.wdtype, s));
-  BEAM_TRY(launch_router_gemm(w.xn32, L.gate_wT, T, 2 * g.N, g.d_pad, w.logits2, s));
-  BEAM_TRY(launch_topk_mask(w.logits2, T, g.N, g.K, g.S, L.mask_threshold, w.ids32, w.gw,
-                            o->topk_ids, o->masked_ids, o->logits, o->weights, o->pre_activation,
-                            o->raw_mask, o->mask, s));
+  BEAM_TRY(strided_input(g, h, h_dtype, T, w, &X, s));
+  BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s));
   prof_mark(1, s);
   BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, T, g.Keff, g.E, block_size, w.plan, s));
   prof_mark(2, s);
-  BEAM_TRY(launch_gateup_simt(L, g, w.xact, w.plan, w.act, s));
-  prof_mark(3, s);
-  BEAM_TRY(launch_down_simt(L, g, w.plan, w.act, w.opair, s));
-  prof_mark(4, s);
+  if (w.tc) {
+    BEAM_TRY(launch_pack_x(X, h_dtype, L.has_norm ? w.inv : nullptr, L.has_norm ? L.norm_w : nullptr, g,
+                           w.plan, w.cap, w.xperm, s));
+    BEAM_TRY(launch_experts_tc(L, g, w.xperm, w.plan, w.cap, w.act16, w.opair, s));
+    prof_mark(3, s);
+    prof_mark(4, s);
+  } else {
+    BEAM_TRY(launch_gateup_simt(L, g, X, h_dtype, T, L.has_norm ? w.inv : nullptr,
+                                L.has_norm ? L.norm_w : nullptr, w.plan, w.act, s));
+    prof_mark(3, s);
+    BEAM_TRY(launch_down_simt(L, g, T, w.plan, w.act, w.opair, s));
+    prof_mark(4, s);
+  }
   BEAM_TRY(launch_combine(w.plan, w.opair, T, g.Keff, g.d, g.d_pad, h, h_dtype, o->out, h_dtype, s));
   prof_mark(5, s);
   return BEAM_OK;
@@ -183,12 +229,9 @@ int beam_gate(const beam_layer_t* layer, const void* h, int h_dtype, int T,
   LayerWs w;
   if (carve(L, T, 0, 1, workspace, &w) > workspace_bytes || !workspace) return BEAM_ERR_WORKSPACE;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  BEAM_TRY(launch_norm_pack(h, h_dtype, T, g.d, g.d_pad, L.has_norm ? L.norm_w : nullptr, w.xn32,
-                            nullptr, L.wdtype, s));
-  BEAM_TRY(launch_router_gemm(w.xn32, L.gate_wT, T, 2 * g.N, g.d_pad, w.logits2, s));
-  BEAM_TRY(launch_topk_mask(w.logits2, T, g.N, g.K, g.S, L.mask_threshold, w.ids32, w.gw,
-                            o->topk_ids, o->masked_ids, o->logits, o->weights, o->pre_activation,
-                            o->raw_mask, o->mask, s));
+  const void* X = nullptr;
+  BEAM_TRY(strided_input(g, h, h_dtype, T, w, &X, s));
+  BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s));
   return BEAM_OK;
 }
 
@@ -205,9 +248,10 @@ int beam_moe_execute(const beam_layer_t* layer, const void* x, int x_dtype, int 
   LayerWs w;
   if (carve(L, T, K, 1, workspace, &w) > workspace_bytes || !workspace) return BEAM_ERR_WORKSPACE;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  BEAM_TRY(launch_norm_pack(x, x_dtype, T, g.d, g.d_pad, nullptr, nullptr, w.xact, L.wdtype, s));
+  const void* X = nullptr;
+  BEAM_TRY(strided_input(g, x, x_dtype, T, w, &X, s));
   BEAM_TRY(launch_permute<int32_t>(ids, wts, T, K, g.E, 1, w.plan, s));
-  BEAM_TRY(launch_experts_simt(L, g, w.xact, w.plan, w.act, w.opair, s));
+  BEAM_TRY(launch_experts_simt(L, g, X, x_dtype, T, w.plan, w.act, w.opair, s));
   BEAM_TRY(launch_combine(w.plan, w.opair, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
   return BEAM_OK;
 }
@@ -265,10 +309,11 @@ int beam_grouped_execute(const beam_layer_t* layer, const void* x, int x_dtype, 
   p.meta = const_cast<int32_t*>(meta);
   p.tok = const_cast<int32_t*>(tokens);
   p.slot = const_cast<int32_t*>(slots);
-  BEAM_TRY(launch_norm_pack(x, x_dtype, T, g.d, g.d_pad, nullptr, nullptr, w.xact, L.wdtype, s));
+  const void* X = nullptr;
+  BEAM_TRY(strided_input(g, x, x_dtype, T, w, &X, s));
   BEAM_TRY(launch_plan_prepare(counts, offsets, tokens, slots, meta, weights_hat, T, K, g.N, p,
                                flags, s));
-  BEAM_TRY(launch_experts_simt(L, g, w.xact, p, w.act, w.opair, s));
+  BEAM_TRY(launch_experts_simt(L, g, X, x_dtype, T, p, w.act, w.opair, s));
   BEAM_TRY(launch_combine(p, w.opair, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
   return BEAM_OK;
 }
@@ -279,11 +324,16 @@ int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w,
   if (T == 0) return BEAM_OK;
   if (!h || !norm_w || !out) return BEAM_ERR_ARG;
   if (h_dtype != BEAM_F32 && h_dtype != BEAM_BF16) return BEAM_ERR_ARG;
-  return status(launch_norm_pack(h, h_dtype, T, d, d, norm_w, out, nullptr, BEAM_F32,
-                                 reinterpret_cast<cudaStream_t>(stream)));
+  return status(launch_rms_norm(h, h_dtype, T, d, norm_w, out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 unsigned long long beam_kernel_launches(void) { return g_launches.load(); }
+
+int beam_set_expert_path(int mode) {
+  if (mode < 0 || mode > 2) return BEAM_ERR_ARG;
+  g_expert_path.store(mode);
+  return BEAM_OK;
+}
 
 int beam_profile_begin(int max_calls) {
   if (max_calls < 1) return BEAM_ERR_ARG;

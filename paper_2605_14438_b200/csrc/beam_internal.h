@@ -46,15 +46,18 @@ cudaError_t record(cudaError_t e);
 void count_launches(int n);  // bookkeeping for beam_kernel_launches()
 
 // gate.cu
-cudaError_t launch_norm_pack(const void* h, int h_dtype, int T, int d, int d_pad,
-                             const float* norm_w, float* xn32, void* xact, int act_dtype,
-                             cudaStream_t s);
-cudaError_t launch_router_gemm(const float* xn32, const float* gate_wT, int T, int cols,
-                               int d_pad, float* L, cudaStream_t s);
-cudaError_t launch_topk_mask(const float* L, int T, int N, int K, int S, float thr,
-                             int32_t* ids32, float* gw, int64_t* topk_ids, int64_t* masked_ids,
-                             float* logits, float* weights, float* pre_act, float* raw_mask,
-                             float* mask, cudaStream_t s);
+cudaError_t launch_pad_rows(const void* h, int h_dtype, int T, int d, int d_pad, void* out,
+                            int out_dtype, cudaStream_t s);
+cudaError_t launch_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w,
+                            float* out, cudaStream_t s);
+int router_splits(int T, int cols, int d_pad);  // split-K factor of launch_router
+cudaError_t launch_router(const void* X, int x_dtype, const float* norm_w, const float* gate_wT,
+                          int T, int cols, int d, int d_pad, float* P, cudaStream_t s);
+cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dtype, int d,
+                             int d_pad, int has_norm, int T, int N, int K, int S, float thr,
+                             float* inv_out, int32_t* ids32, float* gw, int64_t* topk_ids,
+                             int64_t* masked_ids, float* logits, float* weights, float* pre_act,
+                             float* raw_mask, float* mask, cudaStream_t s);
 cudaError_t launch_mask_route(const int64_t* ids, const void* a, int a_dtype, int T, int K,
                               int N, int64_t* out, cudaStream_t s);
 
@@ -68,16 +71,25 @@ cudaError_t launch_plan_prepare(const int32_t* counts, const int32_t* offsets,
                                 const PlanDev& p, int32_t* flags, cudaStream_t s);
 
 // experts_simt.cu
-cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void* xact,
-                               const PlanDev& p, float* act, cudaStream_t s);
-cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, const PlanDev& p,
+cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
+                               const float* inv, const float* nw, const PlanDev& p, float* act,
+                               cudaStream_t s);
+cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const PlanDev& p,
                              const float* act, float* opair, cudaStream_t s);
-inline cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, const void* xact,
-                                       const PlanDev& p, float* act, float* opair, cudaStream_t s) {
-  cudaError_t e = launch_gateup_simt(L, g, xact, p, act, s);
+inline cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, const void* X,
+                                       int x_dtype, int T, const PlanDev& p, float* act, float* opair,
+                                       cudaStream_t s) {
+  cudaError_t e = launch_gateup_simt(L, g, X, x_dtype, T, nullptr, nullptr, p, act, s);
   if (e != cudaSuccess) return e;
-  return launch_down_simt(L, g, p, act, opair, s);
+  return launch_down_simt(L, g, T, p, act, opair, s);
 }
+
+// experts_tc.cu (tcgen05 grouped GEMM, prefill)
+bool tc_supported(const beam_layer_t& L, const Dims& g);
+cudaError_t launch_pack_x(const void* h, int h_dtype, const float* inv, const float* nw, const Dims& g,
+                          const PlanDev& p, int cap, void* xperm, cudaStream_t s);
+cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* xperm, const PlanDev& p,
+                              int cap, void* act16, float* opair, cudaStream_t s);
 
 // combine.cu
 cudaError_t launch_combine(const PlanDev& p, const float* opair, int T, int Keff, int d, int d_pad,

@@ -44,11 +44,36 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
   }
   __syncthreads();
   const int nv = nvalid_s;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    float y = 0.0f;
-    for (int r = 0; r < nv; ++r) y += opair[(size_t)sorted[r] * d_pad + c];
-    if (h != nullptr) y = to_f32<TH>(h[(size_t)t * d + c]) + y;
-    out[(size_t)t * d + c] = from_f32<TO>(y);
+  // one float4 column group per thread; the (up to 8 per batch) expert rows of a
+  // group are loaded back to back, then added in ascending expert order
+  const int d4 = d_pad >> 2;
+  for (int c4 = threadIdx.x; c4 < d4; c4 += blockDim.x) {
+    if (4 * c4 >= d) break;
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r0 = 0; r0 < nv; r0 += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (r0 + q < nv) v[q] = __ldg(reinterpret_cast<const float4*>(opair + (size_t)sorted[r0 + q] * d_pad) + c4);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (r0 + q < nv) {
+          y.x += v[q].x;
+          y.y += v[q].y;
+          y.z += v[q].z;
+          y.w += v[q].w;
+        }
+    }
+    const float yy[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = 4 * c4 + q;
+      if (c < d) {
+        float o = yy[q];
+        if (h != nullptr) o = to_f32<TH>(h[(size_t)t * d + c]) + o;
+        out[(size_t)t * d + c] = from_f32<TO>(o);
+      }
+    }
   }
 }
 

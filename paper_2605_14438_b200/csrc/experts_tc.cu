@@ -1,0 +1,455 @@
+// Grouped SwiGLU experts on the 5th-generation tensor cores (prefill path).
+//
+// Reference: dispatch.grouped_execute (/root/reference/pkg/src/beamoe/dispatch/
+// __init__.py:129-157) -> expert_forward_np (moe.py:96-100):
+//     O_e = (silu(X_e W_gate) * (X_e W_up)) W_down,  y[rows] += O_e * ghat
+//
+// B200 design ("swap AB" grouped GEMM, one persistent kernel per GEMM):
+//   * A = expert weights (UMMA M = 128 weight rows per tile, K-major, bf16),
+//     B = the expert's surviving tokens in plan order (UMMA N = tokens, K-major),
+//     D = fp32 accumulator in TMEM (two 256-column buffers: the epilogue of tile
+//     i overlaps the MMAs of tile i+1).
+//   * Tiles (expert, m-tile, n-tile) are enumerated on the device from the plan
+//     counts — masked slots never become tiles; the MMA N of each tile is the
+//     expert's remaining token count rounded up to 16, so partial tiles cost no
+//     tensor-core work and no B bytes beyond the next 64-row TMA box.
+//   * Warp roles: warp 0 = TMA producer (SWIZZLE_128B boxes into a 4-stage
+//     mbarrier ring), warp 1 = tcgen05.mma issuer (one elected thread,
+//     tcgen05.commit frees smem stages / publishes accumulators), warps 2-5 =
+//     epilogue (tcgen05.ld -> registers -> global).
+//   * GEMM1 (gate/up, K = d): packed rows interleave 16 gate + 16 up rows per
+//     32, so one warp's TMEM lanes hold matching gate/up rows; the epilogue
+//     computes act = silu(g) * u (fp32) and stores bf16 act[pos, f].
+//   * GEMM2 (down, K = f): epilogue scales by the routing weight ghat and stores
+//     fp32 opair[pos, d] for the deterministic ascending-expert combine.
+#include <cuda.h>
+
+#include "beam_common.cuh"
+#include "beam_internal.h"
+
+namespace beam {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int kStages = 4;
+constexpr int kBBox = 64;  // B rows per TMA box
+constexpr int kABytes = BM * BK * 2;
+constexpr int kBBytes = BN * BK * 2;
+constexpr int kBBoxBytes = kBBox * BK * 2;
+constexpr int kTmemCols = 512;
+constexpr int kThreads = 192;
+constexpr int kMaxE = 1024;
+
+struct Args {
+  int mode;  // 0 gate/up, 1 down
+  int E;
+  int m_rows;  // A rows per expert
+  int K;
+  const int32_t* counts;
+  const int32_t* offsets;
+  const float* w;
+  __nv_bfloat16* act;
+  int f_pad;
+  float* opair;
+  int d_pad;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;              // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;    // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+struct Tile {
+  int e, m_tile, a_row0, b_row0, ntok, nmma;
+};
+
+__device__ __forceinline__ Tile decode(int t, const int* tile_off, int E, int MT, const Args& a) {
+  // largest e with tile_off[e] * MT <= t
+  int lo = 0, hi = E;  // invariant: tile_off[lo]*MT <= t < tile_off[hi]*MT
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (tile_off[mid] * MT <= t) lo = mid;
+    else hi = mid;
+  }
+  Tile r;
+  r.e = lo;
+  const int nt = tile_off[lo + 1] - tile_off[lo];
+  const int local = t - tile_off[lo] * MT;
+  r.m_tile = local / nt;
+  const int n_tile = local % nt;
+  r.a_row0 = lo * a.m_rows + r.m_tile * BM;
+  const int tok0 = n_tile * BN;
+  r.ntok = min(BN, a.counts[lo] - tok0);
+  r.b_row0 = a.offsets[lo] + tok0;
+  r.nmma = (r.ntok + 15) & ~15;
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        Args args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;                                  // kStages x 16 KB
+  uint8_t* sb = smem + kStages * kABytes;              // kStages x 32 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kStages * kBBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* tile_off = reinterpret_cast<int*>(tmem_slot + 4);  // [E + 1]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int E = args.E;
+  const int MT = args.m_rows / BM;
+  const int KB = args.K / BK;
+
+  // per-expert n-tile prefix (masked experts: zero tiles)
+  if (warp == 0) {
+    int carry = 0;
+    if (lane == 0) tile_off[0] = 0;
+    for (int base = 0; base < E; base += 32) {
+      const int e = base + lane;
+      int v = e < E ? (args.counts[e] + BN - 1) / BN : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (e < E) tile_off[e + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = tile_off[E] * MT;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const Tile tl = decode(t, tile_off, E, MT, args);
+        const int nbox = (tl.nmma + kBBox - 1) / kBBox;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], kABytes + nbox * kBBoxBytes);
+          tma_load_2d(sa + stage * kABytes, &tmA, &full[stage], kb * BK, tl.a_row0);
+          for (int c = 0; c < nbox; ++c)
+            tma_load_2d(sb + stage * kBBytes + c * kBBoxBytes, &tmB, &full[stage], kb * BK, tl.b_row0 + c * kBBox);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc_base = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const Tile tl = decode(t, tile_off, E, MT, args);
+        const uint32_t idesc = idesc_base | ((uint32_t)(tl.nmma >> 3) << 17);
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        fence_after();
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          const uint64_t ad = sdesc_sw128(smem_u32(sa + stage * kABytes));
+          const uint64_t bd = sdesc_sw128(smem_u32(sb + stage * kBBytes));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          mma_commit(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5 -> TMEM lanes 32*(warp%4)) ----------------
+    const int lane_base = 32 * (warp & 3);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const Tile tl = decode(t, tile_off, E, MT, args);
+      mbar_wait(&tfull[acc], acc_phase);
+      fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + acc * BN;
+      for (int c0 = 0; c0 < tl.ntok; c0 += 32) {
+        float v[32];
+        tmem_ld32(tbase + c0, v);
+        if (args.mode == 0) {
+          // packed rows: lanes 0-15 gate, 16-31 up of features 16*b + (lane & 15)
+          const int b = (tl.m_tile * BM + lane_base) >> 5;
+          const int f = 16 * b + (lane & 15);
+          const bool lo = lane < 16;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float send = lo ? v[16 + j] : v[j];
+            const float r = __shfl_xor_sync(0xffffffffu, send, 16);
+            const float g = lo ? v[j] : r;
+            const float u = lo ? r : v[16 + j];
+            const int col = c0 + (lo ? j : 16 + j);
+            if (col < tl.ntok)
+              args.act[(size_t)(tl.b_row0 + col) * args.f_pad + f] = __float2bfloat16_rn(activation<BEAM_ACT_SILU>(g) * u);
+          }
+        } else {
+          const int row = tl.m_tile * BM + lane_base + lane;  // output channel
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = c0 + j;
+            if (col < tl.ntok) {
+              const int pos = tl.b_row0 + col;
+              args.opair[(size_t)pos * args.d_pad + row] = v[j] * __ldg(args.w + pos);
+            }
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+}
+
+// x_n rows in plan order, bf16 (B operand of GEMM1): X[p] = bf16(h[tok_p] * inv * w)
+template <typename TX>
+__global__ void __launch_bounds__(256) pack_x_kernel(const TX* __restrict__ h, const float* __restrict__ inv,
+                                                     const float* __restrict__ nw, int d, int d_pad,
+                                                     PlanDev p, int cap, __nv_bfloat16* __restrict__ X) {
+  const int total = p.meta[1];
+  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < min(total, cap); row += gridDim.x * 8) {
+    const int tok = p.tok[row];
+    const int lane = threadIdx.x & 31;
+    __nv_bfloat16* dst = X + (size_t)row * d_pad;
+    if (tok < 0) {
+      for (int k = lane * 8; k < d_pad; k += 256) *reinterpret_cast<uint4*>(dst + k) = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const float s = inv ? inv[tok] : 1.0f;
+    const TX* src = h + (size_t)tok * d_pad;
+    for (int k = lane * 8; k < d_pad; k += 256) {
+      float x[8];
+      if constexpr (sizeof(TX) == 2) {
+        unpack<__nv_bfloat16>(ld_cached(src + k), x);
+      } else {
+        unpack<float>(ld_cached(src + k), x);
+        unpack<float>(ld_cached(src + k + 4), x + 4);
+      }
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float a = x[2 * q], b = x[2 * q + 1];
+        if (nw) {
+          const int k0 = k + 2 * q;
+          a = (a * s) * (k0 < d ? __ldg(nw + k0) : 0.0f);
+          b = (b * s) * (k0 + 1 < d ? __ldg(nw + k0 + 1) : 0.0f);
+        }
+        const __nv_bfloat162 v2 = __floats2bfloat162_rn(a, b);
+        o[q] = *reinterpret_cast<const uint32_t*>(&v2);
+      }
+      *reinterpret_cast<uint4*>(dst + k) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static size_t smem_bytes(int E) {
+  return 1024 + (size_t)kStages * (kABytes + kBBytes) + (2 * kStages + 4) * 8 + 16 + (size_t)(E + 1) * 4;
+}
+
+}  // namespace tc
+
+bool tc_supported(const beam_layer_t& L, const Dims& g) {
+  return L.wdtype == BEAM_BF16 && L.activation == BEAM_ACT_SILU && g.d_pad % 128 == 0 &&
+         g.f_pad % 64 == 0 && (2 * g.f_pad) % tc::BM == 0 && g.E <= tc::kMaxE;
+}
+
+cudaError_t launch_pack_x(const void* h, int h_dtype, const float* inv, const float* nw, const Dims& g,
+                          const PlanDev& p, int cap, void* xperm, cudaStream_t s) {
+  const int grid = std::max(1, std::min(num_sms() * 8, (cap + 7) / 8));
+  if (h_dtype == BEAM_BF16)
+    tc::pack_x_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
+  else
+    tc::pack_x_kernel<float><<<grid, 256, 0, s>>>((const float*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* xperm, const PlanDev& p,
+                              int cap, void* act16, float* opair, cudaStream_t s) {
+  using namespace tc;
+  CUtensorMap mA1, mB1, mA2, mB2;
+  if (!make_map(&mA1, L.w_gu, (uint64_t)g.E * 2 * g.f_pad, g.d_pad, BM) ||
+      !make_map(&mB1, xperm, (uint64_t)cap, g.d_pad, kBBox) ||
+      !make_map(&mA2, L.w_down, (uint64_t)g.E * g.d_pad, g.f_pad, BM) ||
+      !make_map(&mB2, act16, (uint64_t)cap, g.f_pad, kBBox))
+    return cudaErrorInvalidValue;
+  const size_t smem = smem_bytes(g.E);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(kMaxE));
+    attr = true;
+  }
+  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
+  grouped_gemm_kernel<<<num_sms(), kThreads, smem, s>>>(mA1, mB1, a1);
+  count_launches(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  Args a2{1, g.E, g.d_pad, g.f_pad, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
+  grouped_gemm_kernel<<<num_sms(), kThreads, smem, s>>>(mA2, mB2, a2);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace beam
