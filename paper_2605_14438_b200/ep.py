@@ -1,0 +1,223 @@
+"""Expert parallelism (EP) for the BEAM layer over torch.distributed.
+
+Not in the reference (expert parallelism is listed as an open limitation,
+PAPER.md:712) — this is the north star's multi-GPU row.
+
+Rank r of P owns the contiguous expert range [r*N/P, (r+1)*N/P).  Every rank
+holds the (small) router and mask router, so gating is replicated; per layer call:
+
+  1. gate the rank's own T tokens (fused sm_100a gating kernel): surviving
+     (token, slot) pairs with their routing weights ghat;
+  2. dispatch: each token is sent ONCE to every rank that owns at least one of its
+     surviving experts (dedup), with a metadata row [K local ids | K weights];
+     masked slots cost no bytes — BEAM's sparsity shrinks the all-to-all;
+  3. the owner runs its local experts on the received rows (beam_moe_execute:
+     masked permute + weight-streaming / tcgen05 experts + combine);
+  4. combine: partial sums travel back; the token's rank adds them in ascending
+     rank order (= ascending expert ranges), then the residual.
+
+Collectives: one all-to-all of P ints (counts; the only host sync) and three
+all_to_all_single calls (rows, metadata, partial sums) — NCCL over NVLink /
+NVSwitch on B200s, gloo in the CPU tests.  Output equals the single-GPU layer up
+to fp32 re-association of the per-token sum across ranks.
+
+The exchange logic is device-agnostic and takes the gating and local-expert
+compute as callables, so tests/test_ep_gloo.py runs it with world_size 2 on CPU
+with the oracle as the local compute.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib, _runtime
+
+
+@dataclass
+class Gated:
+    xn: torch.Tensor     # [T, d] normalised activations (what the experts consume)
+    ids: torch.Tensor    # [T, K] int64 surviving expert ids, -1 = masked
+    ghat: torch.Tensor   # [T, K] f32 routing weight of each slot (0 where masked)
+
+
+def ep_exchange_forward(h: torch.Tensor, gated: Gated, num_experts: int, local_fn, group=None) -> torch.Tensor:
+    """Steps 2-4 above.  ``local_fn(x [n, d], ids [n, K] int32 local ids (-1 skip),
+    w [n, K] f32) -> y [n, d] f32`` runs this rank's experts.  Returns h + y in
+    h's dtype."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if num_experts % world:
+        raise ValueError("num_experts must divide evenly across ranks")
+    n_local = num_experts // world
+    t, k = gated.ids.shape
+    dev = h.device
+    ids = gated.ids
+    dest = torch.where(ids >= 0, ids // n_local, torch.full_like(ids, -1))            # [T, K]
+    send_mask = torch.stack([(dest == r).any(dim=1) for r in range(world)])             # [P, T]
+    pairs = send_mask.nonzero()                                                          # (r, t) rank-major
+    r_idx, t_idx = pairs[:, 0], pairs[:, 1]
+    counts_send = send_mask.sum(dim=1).to(torch.int64)
+    # metadata: local ids of the slots that belong to the destination, and their weights
+    mine = dest[t_idx] == r_idx[:, None]                                                 # [n, K]
+    loc_ids = torch.where(mine, ids[t_idx] - r_idx[:, None] * n_local, torch.full_like(ids[t_idx], -1))
+    loc_w = torch.where(mine, gated.ghat[t_idx], torch.zeros_like(gated.ghat[t_idx]))
+    meta = torch.cat([loc_ids.to(torch.int32), loc_w.to(torch.float32).view(torch.int32)], dim=1).contiguous()
+    x_send = gated.xn[t_idx].contiguous()
+
+    counts_recv = torch.empty_like(counts_send)
+    dist.all_to_all_single(counts_recv, counts_send, group=group)
+    send_splits = counts_send.tolist()
+    recv_splits = counts_recv.tolist()
+    n_recv = int(sum(recv_splits))
+    x_recv = torch.empty((n_recv, x_send.shape[1]), dtype=x_send.dtype, device=dev)
+    meta_recv = torch.empty((n_recv, 2 * k), dtype=torch.int32, device=dev)
+    dist.all_to_all_single(x_recv, x_send, recv_splits, send_splits, group=group)
+    dist.all_to_all_single(meta_recv, meta, recv_splits, send_splits, group=group)
+
+    ids_recv = meta_recv[:, :k].contiguous()
+    w_recv = meta_recv[:, k:].contiguous().view(torch.float32)
+    y_recv = local_fn(x_recv, ids_recv, w_recv) if n_recv else torch.zeros((0, x_send.shape[1]), device=dev)
+    y_recv = y_recv.to(torch.float32).contiguous()
+
+    y_back = torch.empty((int(sum(send_splits)), y_recv.shape[1]), dtype=torch.float32, device=dev)
+    dist.all_to_all_single(y_back, y_recv, send_splits, recv_splits, group=group)
+
+    # ascending rank == ascending expert range; each rank's rows have unique tokens
+    y = torch.zeros((t, h.shape[1]), dtype=torch.float32, device=dev)
+    start = 0
+    for r in range(world):
+        n = send_splits[r]
+        if n:
+            y[t_idx[start : start + n]] += y_back[start : start + n]
+        start += n
+    return (h.to(torch.float32) + y).to(h.dtype)
+
+
+class EPBeamLayer:
+    """One BEAM MoE layer sharded over the ranks of ``group`` (CUDA + NCCL).
+
+    ``block`` is a full-size ``MoEBlock`` description used only for its routers /
+    norm (replicated); only this rank's experts are kept on the device."""
+
+    def __init__(self, block, group=None):
+        from .moe import MoEBlock, MoEBlockConfig
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        cfg = block.cfg
+        if cfg.num_experts % self.world:
+            raise ValueError("num_experts must divide evenly across ranks")
+        if cfg.num_shared:
+            raise ValueError("shared experts are not sharded by the EP path")
+        self.cfg = cfg
+        self.n_local = cfg.num_experts // self.world
+        self.block = block
+        lo = self.rank * self.n_local
+        lcfg = MoEBlockConfig(cfg.d_h, cfg.d_ff, self.n_local, 1, 0, False, cfg.activation)
+        self.local = MoEBlock(lcfg, dtype=block.dtype, device=block.device, _empty=True)
+        self.local.w_gu.copy_(block.w_gu[lo : lo + self.n_local])
+        self.local.w_down.copy_(block.w_down[lo : lo + self.n_local])
+
+    def gate(self, h: torch.Tensor) -> Gated:
+        from .beam import _threshold
+        from .moe import _gate_call  # noqa: F401  (same C entry, full router)
+
+        blk = self.block
+        desc = blk.layer_desc(_threshold(blk.mask_router.tau))
+        t = h.shape[0]
+        n, k = self.cfg.num_experts, self.cfg.top_k
+        masked = torch.empty(t, k, dtype=torch.int64, device=h.device)
+        weights = torch.empty(t, n, dtype=torch.float32, device=h.device)
+        o = _lib.Outputs()
+        o.masked_ids = masked.data_ptr()
+        o.weights = weights.data_ptr()
+        lib = _lib.load()
+        ws = _runtime.workspace(lib.beam_workspace_bytes(ctypes.byref(desc), t, 0, 1), h.device)
+        _lib.check(lib.beam_gate(ctypes.byref(desc), h.data_ptr(),
+                                 _lib.BEAM_BF16 if h.dtype == torch.bfloat16 else _lib.BEAM_F32, t,
+                                 ctypes.byref(o), ws.data_ptr(), ws.numel(), _runtime.stream_handle(h.device)),
+                   "beam_gate")
+        ghat = torch.where(masked >= 0, torch.gather(weights, 1, masked.clamp(min=0)), torch.zeros((), device=h.device))
+        xn = blk.normalize(h).to(blk.dtype) if blk.norm_w is not None else h.to(blk.dtype)
+        return Gated(xn=xn, ids=masked, ghat=ghat)
+
+    def local_fn(self, x, ids, w):
+        from .dispatch import execute_routed
+
+        return execute_routed(self.local, x.contiguous(), ids.contiguous(), w.contiguous())
+
+    def forward(self, h: torch.Tensor) -> torch.Tensor:
+        h = h.contiguous()
+        return ep_exchange_forward(h, self.gate(h), self.cfg.num_experts, self.local_fn, self.group)
+
+
+# ---------------------------------------------------------------------------
+# bench.py --gpus N (torchrun): EP at the Qwen3-30B-A3B shape, T tokens per rank
+# ---------------------------------------------------------------------------
+
+
+def bench_main(args, bench):
+    import json
+
+    import paper_2605_14438_b200 as B
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    q = bench.Q30
+    cfg = B.MoEBlockConfig(d_h=q["d"], d_ff=q["f"], num_experts=q["n"], top_k=q["k"])
+    w = bench.make_layer0()
+    h = bench.make_tokens(args.tokens, 7 + rank)
+    theta = bench.calibrate_theta(bench.make_tokens(args.tokens, 7), w["router"], w["mask"], q["k"], args.sparsity)
+    blk = B.MoEBlock.from_weights(cfg, w["router"], (w["wg"], w["wu"], w["wd"]),
+                                  mask_w=bench.mask_with_theta(w["mask"], theta), dtype=torch.bfloat16, device=dev)
+    layer = EPBeamLayer(blk)
+    # only the local shard stays resident (the gate never reads expert weights)
+    blk.w_gu = torch.zeros(1, dtype=torch.bfloat16, device=dev)
+    blk.w_down = torch.zeros(1, dtype=torch.bfloat16, device=dev)
+    x = h.to(dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        layer.forward(x)
+    torch.cuda.synchronize()
+    dist.barrier()
+    total = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        layer.forward(x)
+        e.record()
+        e.synchronize()
+        total += s.elapsed_time(e)
+    t_max = torch.tensor([total], device=dev)
+    dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item()) / args.steps
+    if rank == 0:
+        line = {
+            "metric": bench.METRIC, "value": world * args.tokens / (ms / 1e3), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": f"Qwen3-30B-A3B MoE layer, expert parallel EP{world}, T={args.tokens} tokens/rank, "
+                                   f"s={args.sparsity}", **q, "parallelism": f"ep{world}",
+                       "experts_per_rank": q["n"] // world, "l2": "flushed before every step",
+                       "timing": "CUDA events per step, max over ranks"},
+            "gpu_launches": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
