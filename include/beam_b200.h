@@ -30,8 +30,10 @@
  * Conventions: all pointers are DEVICE pointers unless stated; every entry
  * launches on `stream` only, never allocates, never synchronises the host, and
  * returns BEAM_OK or a negative status.  Scratch comes from the caller's
- * workspace (size from beam_workspace_bytes).  Results are deterministic and
- * independent of grid size (no floating-point atomics).
+ * workspace (size from beam_workspace_bytes); the workspace must be zero-filled
+ * once before its first use (it holds grid-completion counters that every call
+ * leaves at zero — re-zero it after a failed call).  Results are deterministic
+ * and independent of grid size (no floating-point atomics).
  */
 #ifndef BEAM_B200_H
 #define BEAM_B200_H

@@ -23,7 +23,9 @@ def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
         buf = _workspaces.get(key)
         if buf is None or buf.numel() < nbytes:
             size = max(nbytes, int(buf.numel() * 1.5) if buf is not None else 0, 1 << 20)
-            buf = torch.empty(size, dtype=torch.uint8, device=device)
+            # zero-filled once: the grid-completion counters at its start must
+            # begin at 0 (the kernels reset them after every use)
+            buf = torch.zeros(size, dtype=torch.uint8, device=device)
             _workspaces[key] = buf
         return buf
 

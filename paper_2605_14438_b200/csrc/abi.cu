@@ -76,6 +76,8 @@ static bool use_tc(const beam_layer_t& L, const Dims& g, int T, int Krow) {
 struct LayerWs {
   bool tc;
   int cap;
+  int* counters;   // [64] grid-completion counters (zero-initialised workspace; reset after use)
+  int* pscratch;   // multi-CTA permute scratch (its first 64 ints are a counter)
   void* xperm;     // [cap, d_pad] bf16 x_n in plan order (tc path)
   void* act16;     // [cap, f_pad] bf16 (tc path)
   void* xpad;      // [T, d_pad] input rows re-strided (only when d_h % 8 != 0)
@@ -97,6 +99,8 @@ static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, La
   const size_t cap = M + (size_t)g.E * (size_t)(bs > 0 ? bs - 1 : 0);
   Carver c(ws);
   LayerWs w;
+  w.counters = c.take<int>(64);
+  w.pscratch = c.take<int>(permute_scratch_bytes(T, Krow, g.E) / sizeof(int));
   w.tc = use_tc(L, g, T, Krow);
   w.cap = (int)cap;
   w.xperm = w.tc ? c.take<__nv_bfloat16>(cap * g.d_pad) : nullptr;
@@ -164,16 +168,35 @@ size_t beam_workspace_bytes(const beam_layer_t* layer, int T, int K, int block_s
   return carve(*layer, T, K, block_size < 1 ? 1 : block_size, nullptr, nullptr);
 }
 
+static TopkArgs topk_args(const beam_layer_t& L, const Dims& g, const beam_outputs_t* o, LayerWs& w) {
+  TopkArgs a;
+  a.N = g.N;
+  a.K = g.K;
+  a.S = g.S;
+  a.thr = L.mask_threshold;
+  a.has_norm = L.has_norm;
+  a.d = g.d;
+  a.d_pad = g.d_pad;
+  a.inv_out = w.inv;
+  a.ids32 = w.ids32;
+  a.gw = w.gw;
+  a.topk_ids = o->topk_ids;
+  a.masked_ids = o->masked_ids;
+  a.logits = o->logits;
+  a.weights = o->weights;
+  a.pre_act = o->pre_activation;
+  a.raw_mask = o->raw_mask;
+  a.mask = o->mask;
+  return a;
+}
+
 // The gating half shared by beam_layer_forward and beam_gate.
 static cudaError_t run_gate(const beam_layer_t& L, const Dims& g, const void* X, int h_dtype, int T,
                             const beam_outputs_t* o, LayerWs& w, cudaStream_t s) {
   const float* nw = L.has_norm ? L.norm_w : nullptr;
   cudaError_t e = launch_router(X, h_dtype, nw, L.gate_wT, T, 2 * g.N, g.d, g.d_pad, w.logits2, s);
   if (e != cudaSuccess) return e;
-  return launch_topk_mask(w.logits2, router_splits(T, 2 * g.N, g.d_pad), X, h_dtype, g.d, g.d_pad,
-                          L.has_norm, T, g.N, g.K, g.S, L.mask_threshold, w.inv, w.ids32, w.gw,
-                          o->topk_ids, o->masked_ids, o->logits, o->weights, o->pre_activation,
-                          o->raw_mask, o->mask, s);
+  return launch_topk_mask(w.logits2, router_splits(T, 2 * g.N, g.d_pad), X, h_dtype, T, topk_args(L, g, o, w), s);
 }
 
 int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, int T,
@@ -194,9 +217,16 @@ int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, in
 
   prof_mark(0, s);
   BEAM_TRY(strided_input(g, h, h_dtype, T, w, &X, s));
-  BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s));
-  prof_mark(1, s);
-  BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, T, g.Keff, g.E, block_size, w.plan, s));
+  if (gate_fused_supported(T, g.N, g.E, g.d_pad)) {
+    // decode: projection + top-K + permute in one launch
+    BEAM_TRY(launch_gate_fused(X, h_dtype, L.has_norm ? L.norm_w : nullptr, L.gate_wT, T, g.d, g.d_pad,
+                               w.logits2, topk_args(L, g, o, w), g.E, block_size, w.plan, w.counters, s));
+    prof_mark(1, s);
+  } else {
+    BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s));
+    prof_mark(1, s);
+    BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, T, g.Keff, g.E, block_size, w.plan, w.pscratch, s));
+  }
   prof_mark(2, s);
   if (w.tc) {
     BEAM_TRY(launch_pack_x(X, h_dtype, L.has_norm ? w.inv : nullptr, L.has_norm ? L.norm_w : nullptr, g,
@@ -250,7 +280,7 @@ int beam_moe_execute(const beam_layer_t* layer, const void* x, int x_dtype, int 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const void* X = nullptr;
   BEAM_TRY(strided_input(g, x, x_dtype, T, w, &X, s));
-  BEAM_TRY(launch_permute<int32_t>(ids, wts, T, K, g.E, 1, w.plan, s));
+  BEAM_TRY(launch_permute<int32_t>(ids, wts, T, K, g.E, 1, w.plan, w.pscratch, s));
   BEAM_TRY(launch_experts_simt(L, g, X, x_dtype, T, w.plan, w.act, w.opair, s));
   BEAM_TRY(launch_combine(w.plan, w.opair, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
   return BEAM_OK;
@@ -280,7 +310,7 @@ int beam_group_by_expert(const int64_t* ids, int T, int K, int N, int block_size
   p.meta = meta;
   p.tok = tokens;
   p.slot = slots;
-  return status(launch_permute<int64_t>(ids, nullptr, T, K, N, block_size, p,
+  return status(launch_permute<int64_t>(ids, nullptr, T, K, N, block_size, p, nullptr,
                                         reinterpret_cast<cudaStream_t>(stream)));
 }
 

@@ -41,6 +41,19 @@ struct PlanDev {
   int32_t* slot_expert;  // [T*Keff] expert of (t,k), -1 if dropped
 };
 
+// Arguments of the per-token top-K / softmax / mask step (route_device.cuh).
+struct TopkArgs {
+  int N, K, S;  // routed experts, top-k, shared experts (always-on slots K..K+S-1)
+  float thr;    // keep iff a >= thr
+  int has_norm, d, d_pad;
+  float* inv_out;  // [T] inverse RMS (for the expert kernels)
+  int32_t* ids32;  // [T, K+S] masked ids (int32), -1 = dropped
+  float* gw;       // [T, K+S] ghat per slot
+  int64_t* topk_ids;
+  int64_t* masked_ids;
+  float *logits, *weights, *pre_act, *raw_mask, *mask;  // dense [T, N] (optional)
+};
+
 int num_sms();
 cudaError_t record(cudaError_t e);
 void count_launches(int n);  // bookkeeping for beam_kernel_launches()
@@ -53,18 +66,22 @@ cudaError_t launch_rms_norm(const void* h, int h_dtype, int T, int d, const floa
 int router_splits(int T, int cols, int d_pad);  // split-K factor of launch_router
 cudaError_t launch_router(const void* X, int x_dtype, const float* norm_w, const float* gate_wT,
                           int T, int cols, int d, int d_pad, float* P, cudaStream_t s);
-cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dtype, int d,
-                             int d_pad, int has_norm, int T, int N, int K, int S, float thr,
-                             float* inv_out, int32_t* ids32, float* gw, int64_t* topk_ids,
-                             int64_t* masked_ids, float* logits, float* weights, float* pre_act,
-                             float* raw_mask, float* mask, cudaStream_t s);
+cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dtype, int T,
+                             const TopkArgs& a, cudaStream_t s);
+bool gate_fused_supported(int T, int N, int E, int d_pad);
+cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, const float* gate_wT, int T,
+                              int d, int d_pad, float* P, const TopkArgs& a, int E, int bs,
+                              const PlanDev& p, int* counters, cudaStream_t s);
 cudaError_t launch_mask_route(const int64_t* ids, const void* a, int a_dtype, int T, int K,
                               int N, int64_t* out, cudaStream_t s);
 
 // permute.cu
+// scratch: permute_scratch_bytes() bytes, zero-initialised once (multi-CTA path
+// for large T*K; the kernels leave it reusable).  nullptr -> single-CTA path.
+size_t permute_scratch_bytes(int T, int K, int E);
 template <typename IdT>
 cudaError_t launch_permute(const IdT* ids, const float* w, int T, int K, int E, int bs,
-                           const PlanDev& p, cudaStream_t s);
+                           const PlanDev& p, int* scratch, cudaStream_t s);
 cudaError_t launch_plan_prepare(const int32_t* counts, const int32_t* offsets,
                                 const int32_t* tokens, const int32_t* slots, const int32_t* meta,
                                 const float* weights_hat, int T, int K, int N,

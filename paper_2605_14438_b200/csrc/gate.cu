@@ -16,29 +16,9 @@
 // kernels stream h (bf16/f32) against W*w and the top-K kernel (one warp per
 // token) computes inv_rms from the same h row, applies it, selects, and writes
 // inv_rms for the expert kernels, which normalise x on load.
-#include "beam_common.cuh"
-#include "beam_internal.h"
+#include "route_device.cuh"
 
 namespace beam {
-
-// 4 consecutive elements (k % 4 == 0) as float4
-template <typename T> __device__ __forceinline__ float4 ld4(const T* p);
-template <> __device__ __forceinline__ float4 ld4<float>(const float* p) {
-  return __ldg(reinterpret_cast<const float4*>(p));
-}
-template <> __device__ __forceinline__ float4 ld4<__nv_bfloat16>(const __nv_bfloat16* p) {
-  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-  return make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
-                     __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u));
-}
-
-// norm weights at k..k+3 (zero beyond d; NULL -> ones)
-__device__ __forceinline__ float4 ld_norm4(const float* __restrict__ nw, int k, int d) {
-  if (nw == nullptr) return make_float4(1.f, 1.f, 1.f, 1.f);
-  if (k + 3 < d && (d & 3) == 0) return __ldg(reinterpret_cast<const float4*>(nw + k));
-  return make_float4(k < d ? nw[k] : 0.f, k + 1 < d ? nw[k + 1] : 0.f, k + 2 < d ? nw[k + 2] : 0.f,
-                     k + 3 < d ? nw[k + 3] : 0.f);
-}
 
 // ---------------------------------------------------------------------------
 // 0. pad / convert rows to stride d_pad (only when d_h is not a multiple of 8)
@@ -178,23 +158,23 @@ __global__ void __launch_bounds__(256) router_gemm_kernel(const TX* __restrict__
 
 // ---------------------------------------------------------------------------
 // 2b. Decode projection (T <= 64): split-K weight-streaming GEMV.  Each warp owns
-//     2 columns of W and a k-range, keeps 32 tokens x 2 fp32 accumulators in
-//     registers, streams W once per 32-token tile with 16-byte loads and reads h
-//     through L1.  Partials go to P[split][T][cols]; the top-K kernel adds the
-//     splits in a fixed order (deterministic).
+//     2 columns of W and a k-range; the CTA stages its 32-token tile of h for that
+//     k-range in shared memory with all loads in flight, every warp issues all of
+//     its weight loads up front, then accumulates 32 tokens x 2 columns in
+//     registers.  Partials go to P[split][T][cols]; consumers add the splits in a
+//     fixed order (deterministic).
 // ---------------------------------------------------------------------------
 constexpr int kGemvCols = 2;
 constexpr int kGemvTT = 32;
-constexpr int kGemvK = 128;  // k elements per lane-row step (32 lanes x 4)
+constexpr int kGemvK = 128;      // k elements per lane-row step (32 lanes x 4)
+constexpr int kGemvSteps = 8;    // kr <= 1024
+constexpr int kFusedMaxSplit = 4;
 
 template <typename TX>
-__global__ void __launch_bounds__(256) router_gemv_kernel(const TX* __restrict__ X,
-                                                          const float* __restrict__ nw,
-                                                          const float* __restrict__ W, int T,
-                                                          int cols, int d, int d_pad, int kr,
-                                                          float* __restrict__ P) {
-  extern __shared__ float xs[];  // [kGemvTT][kr] fp32 token tile of this k-range
-  __shared__ float red_s[8][kGemvCols * kGemvTT];
+__device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const float* __restrict__ nw,
+                                                 const float* __restrict__ W, int T, int cols, int d,
+                                                 int d_pad, int kr, float* __restrict__ P, float* xs,
+                                                 float* red_s) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int c0 = (blockIdx.x * 8 + wib) * kGemvCols;
   const int split = blockIdx.y;
@@ -202,19 +182,15 @@ __global__ void __launch_bounds__(256) router_gemv_kernel(const TX* __restrict__
   const int nt = min(kGemvTT, T - t0);
   const int ks = split * kr, ke = min(d_pad, ks + kr);
   const int kn = ke - ks;
-  // stage the token tile: every thread issues its loads before any use
   for (int v = threadIdx.x; v < nt * (kn >> 2); v += 256) {
     const int t = v / (kn >> 2), k4 = v % (kn >> 2);
-    const float4 x = ld4<TX>(X + (size_t)(t0 + t) * d_pad + ks + 4 * k4);
-    *reinterpret_cast<float4*>(xs + t * kr + 4 * k4) = x;
+    *reinterpret_cast<float4*>(xs + t * kr + 4 * k4) = ld4<TX>(X + (size_t)(t0 + t) * d_pad + ks + 4 * k4);
   }
-  // this warp's weight chunks (all in flight at once)
-  constexpr int kMaxSteps = 8;  // kr <= 8 * 128
-  float4 wa[kMaxSteps], wb[kMaxSteps];
+  float4 wa[kGemvSteps], wb[kGemvSteps];
   const float* w0 = W + (size_t)min(c0, cols - 1) * d_pad;
   const float* w1 = W + (size_t)min(c0 + 1, cols - 1) * d_pad;
 #pragma unroll
-  for (int i = 0; i < kMaxSteps; ++i) {
+  for (int i = 0; i < kGemvSteps; ++i) {
     const int k = ks + 4 * lane + kGemvK * i;
     if (k < ke) {
       wa[i] = __ldg(reinterpret_cast<const float4*>(w0 + k));
@@ -229,8 +205,8 @@ __global__ void __launch_bounds__(256) router_gemv_kernel(const TX* __restrict__
 #pragma unroll
   for (int i = 0; i < kGemvCols * kGemvTT; ++i) acc[i] = 0.0f;
 #pragma unroll
-  for (int i = 0; i < kMaxSteps; ++i) {
-    const int kk = 4 * lane + kGemvK * i;  // offset inside the k-range
+  for (int i = 0; i < kGemvSteps; ++i) {
+    const int kk = 4 * lane + kGemvK * i;
     if (ks + kk < ke) {
       const float4 a = wa[i], b = wb[i];
 #pragma unroll
@@ -246,42 +222,59 @@ __global__ void __launch_bounds__(256) router_gemv_kernel(const TX* __restrict__
       }
     }
   }
-  warp_reduce_to_smem<kGemvCols * kGemvTT>(acc, red_s[wib], lane);
+  warp_reduce_to_smem<kGemvCols * kGemvTT>(acc, red_s + wib * kGemvCols * kGemvTT, lane);
   if (c0 < cols) {
     for (int i = lane; i < kGemvCols * kGemvTT; i += 32) {
       const int j = i / kGemvTT, t = i % kGemvTT;
-      if (t < nt && c0 + j < cols) P[((size_t)split * T + t0 + t) * cols + c0 + j] = red_s[wib][i];
+      if (t < nt && c0 + j < cols) P[((size_t)split * T + t0 + t) * cols + c0 + j] = red_s[wib * kGemvCols * kGemvTT + i];
     }
   }
 }
 
-static int gemv_kr(int T, int cols, int d_pad) {
+template <typename TX>
+__global__ void __launch_bounds__(256) router_gemv_kernel(const TX* __restrict__ X,
+                                                          const float* __restrict__ nw,
+                                                          const float* __restrict__ W, int T,
+                                                          int cols, int d, int d_pad, int kr,
+                                                          float* __restrict__ P) {
+  extern __shared__ float xs[];
+  __shared__ float red_s[8 * kGemvCols * kGemvTT];
+  router_gemv_body<TX>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s);
+}
+
+// k-range per split: enough CTAs to cover the SMs, kr <= kGemvSteps * 128
+static int gemv_kr(int T, int cols, int d_pad, int max_split) {
   const int col_ctas = ceil_div(cols, 8 * kGemvCols);
   const int tok_ctas = ceil_div(T, kGemvTT);
   int s = ceil_div(num_sms(), col_ctas * tok_ctas);
-  const int smax = ceil_div(d_pad, kGemvK);
-  const int smin = ceil_div(d_pad, 8 * kGemvK);  // kr <= 1024 (registers / smem)
-  if (s < smin) s = smin;
-  s = s < 1 ? 1 : (s > smax ? smax : s);
+  const int smin = ceil_div(d_pad, kGemvSteps * kGemvK);
+  s = std::min(s, max_split);
+  s = std::min(s, ceil_div(d_pad, kGemvK));
+  s = std::max(s, smin);
   return ceil_div(ceil_div(d_pad, s), kGemvK) * kGemvK;
 }
 
 int router_splits(int T, int cols, int d_pad) {
   if (T > 64) return 1;
-  return ceil_div(d_pad, gemv_kr(T, cols, d_pad));
+  return ceil_div(d_pad, gemv_kr(T, cols, d_pad, 1 << 20));
+}
+
+template <typename K>
+static void set_smem(K kernel, int bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 cudaError_t launch_router(const void* X, int x_dtype, const float* norm_w, const float* gate_wT,
                           int T, int cols, int d, int d_pad, float* P, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (T <= 64) {
-    const int kr = gemv_kr(T, cols, d_pad);
+    const int kr = gemv_kr(T, cols, d_pad, 1 << 20);
     dim3 grid(ceil_div(cols, 8 * kGemvCols), ceil_div(d_pad, kr), ceil_div(T, kGemvTT));
     const size_t smem = (size_t)kGemvTT * kr * sizeof(float);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(router_gemv_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(router_gemv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      set_smem(router_gemv_kernel<__nv_bfloat16>, kGemvTT * kGemvSteps * kGemvK * 4);
+      set_smem(router_gemv_kernel<float>, kGemvTT * kGemvSteps * kGemvK * 4);
       attr = true;
     }
     if (x_dtype == BEAM_BF16)
@@ -300,152 +293,124 @@ cudaError_t launch_router(const void* X, int x_dtype, const float* norm_w, const
 }
 
 // ---------------------------------------------------------------------------
-// 3. Top-K + softmax + mask: one warp per token, N <= 32 * kMaxPerLane.
-//    Computes inv_rms from the token's h row, sums the projection partials,
-//    selects the K largest (desc value, asc index), writes everything.
+// 3. Stand-alone top-K + softmax + mask (prefill / wide N): one warp per token.
 // ---------------------------------------------------------------------------
-constexpr int kMaxPerLane = 16;  // N <= 512
-
-template <typename TX>
-__global__ void __launch_bounds__(128) topk_mask_kernel(
-    const float* __restrict__ L, int splits, const TX* __restrict__ X, int d, int d_pad,
-    int has_norm, int T, int N, int K, int S, float thr, float* __restrict__ inv_out,
-    int32_t* __restrict__ ids32, float* __restrict__ gw, int64_t* __restrict__ topk_ids,
-    int64_t* __restrict__ masked_ids, float* __restrict__ logits, float* __restrict__ weights,
-    float* __restrict__ pre_act, float* __restrict__ raw_mask, float* __restrict__ mask) {
+template <typename TX, int NPL>
+__global__ void __launch_bounds__(128) topk_mask_kernel(const float* __restrict__ L, int splits,
+                                                        const TX* __restrict__ X, int T, TopkArgs a) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
   if (t >= T) return;
-  const int Keff = K + S;
-
-  float inv = 1.0f;
-  if (has_norm) {  // tensor.py:485-487: (mean(x^2) + eps)^-1/2 over the real d entries
-    const TX* row = X + (size_t)t * d_pad;
-    float ss = 0.0f;
-#pragma unroll 8
-    for (int k = 4 * lane; k < d_pad; k += 128) {
-      const float4 x = ld4<TX>(row + k);
-      ss = fmaf(x.x, x.x, ss);
-      ss = fmaf(x.y, x.y, ss);
-      ss = fmaf(x.z, x.z, ss);
-      ss = fmaf(x.w, x.w, ss);
-    }
-    ss = warp_sum(ss);
-    inv = 1.0f / sqrtf(ss / (float)d + 1e-6f);
-  }
-  if (inv_out && lane == 0) inv_out[t] = inv;
-
-  // router logits v and mask pre-activations av of this lane's experts, summed
-  // over the split-K partials in split order (all loads of a split in flight)
-  float v[kMaxPerLane], av[kMaxPerLane];
-  int rank[kMaxPerLane];
-#pragma unroll
-  for (int i = 0; i < kMaxPerLane; ++i) {
-    v[i] = 0.0f;
-    av[i] = 0.0f;
-    rank[i] = -1;
-  }
-  for (int sp = 0; sp < splits; ++sp) {
-    const float* row = L + ((size_t)sp * T + t) * 2 * N;
-#pragma unroll
-    for (int i = 0; i < kMaxPerLane; ++i) {
-      const int j = lane + 32 * i;
-      if (j < N) {
-        v[i] += row[j];
-        av[i] += row[N + j];
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < kMaxPerLane; ++i) {
-    v[i] *= inv;
-    av[i] *= inv;
-  }
-
-  float top_val = 0.0f;
-  for (int r = 0; r < K; ++r) {
-    bool have = false;
-    float bv = 0.0f;
-    int bj = 0x7fffffff;
-#pragma unroll
-    for (int i = 0; i < kMaxPerLane; ++i) {
-      const int j = lane + 32 * i;
-      if (j < N && rank[i] < 0) {
-        if (!have || v[i] > bv) {  // j ascending within a lane: ties keep the lower j
-          have = true;
-          bv = v[i];
-          bj = j;
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-      const bool ohave = __shfl_xor_sync(0xffffffffu, (int)have, o) != 0;
-      const bool better = ohave && (!have || ov > bv || (ov == bv && oj < bj));
-      if (better) {
-        bv = ov;
-        bj = oj;
-        have = true;
-      }
-    }
-    if (r == 0) top_val = bv;
-#pragma unroll
-    for (int i = 0; i < kMaxPerLane; ++i)
-      if (lane + 32 * i == bj) rank[i] = r;
-  }
-
-  // softmax over the K kept logits (tensor.py:440-451): exp(l - max) / sum
-  float part = 0.0f;
-#pragma unroll
-  for (int i = 0; i < kMaxPerLane; ++i)
-    if (rank[i] >= 0) part += expf(v[i] - top_val);
-  const float denom = warp_sum(part);
-
-#pragma unroll
-  for (int i = 0; i < kMaxPerLane; ++i) {
-    const int j = lane + 32 * i;
-    if (j >= N) continue;
-    const float a = av[i];
-    const bool keep = a >= thr;  // NaN -> false
-    const float g = rank[i] >= 0 ? expf(v[i] - top_val) / denom : 0.0f;
-    if (rank[i] >= 0) {
-      const int r = rank[i];
-      const size_t o = (size_t)t * Keff + r;
-      ids32[o] = keep ? j : -1;
-      gw[o] = keep ? g : 0.0f;
-      if (topk_ids) topk_ids[(size_t)t * K + r] = j;
-      if (masked_ids) masked_ids[(size_t)t * K + r] = keep ? j : -1;
-    }
-    const size_t od = (size_t)t * N + j;
-    if (logits) logits[od] = v[i];
-    if (weights) weights[od] = g;
-    if (pre_act) pre_act[od] = a;
-    if (raw_mask) raw_mask[od] = sigmoid_ref(a);
-    if (mask) mask[od] = keep ? 1.0f : 0.0f;
-  }
-  // shared experts: always-on slots K..K+S-1, weight 1.0 (beam.py:163-164)
-  for (int s = lane; s < S; s += 32) {
-    const size_t o = (size_t)t * Keff + K + s;
-    ids32[o] = N + s;
-    gw[o] = 1.0f;
-  }
+  topk_token<TX, NPL, 16, false>(L, splits, T, X, t, threadIdx.x & 31, a);
 }
 
-cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dtype, int d,
-                             int d_pad, int has_norm, int T, int N, int K, int S, float thr,
-                             float* inv_out, int32_t* ids32, float* gw, int64_t* topk_ids,
-                             int64_t* masked_ids, float* logits, float* weights, float* pre_act,
-                             float* raw_mask, float* mask, cudaStream_t s) {
-  if (T <= 0) return cudaSuccess;
+template <typename TX>
+static void topk_dispatch(const float* L, int splits, const void* X, int T, const TopkArgs& a, cudaStream_t s) {
   const int grid = ceil_div(T, 4);
-  if (x_dtype == BEAM_BF16)
-    topk_mask_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(L, splits, (const __nv_bfloat16*)X, d, d_pad, has_norm, T, N, K, S, thr, inv_out, ids32, gw, topk_ids, masked_ids, logits, weights, pre_act, raw_mask, mask);
-  else
-    topk_mask_kernel<float><<<grid, 128, 0, s>>>(L, splits, (const float*)X, d, d_pad, has_norm, T, N, K, S, thr, inv_out, ids32, gw, topk_ids, masked_ids, logits, weights, pre_act, raw_mask, mask);
+  const int npl = ceil_div(a.N, 32);
+  if (npl <= 1) topk_mask_kernel<TX, 1><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
+  else if (npl <= 2) topk_mask_kernel<TX, 2><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
+  else if (npl <= 4) topk_mask_kernel<TX, 4><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
+  else if (npl <= 8) topk_mask_kernel<TX, 8><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
+  else topk_mask_kernel<TX, 16><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
+}
+
+cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dtype, int T,
+                             const TopkArgs& a, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  if (splits > 16) return cudaErrorInvalidValue;
+  if (x_dtype == BEAM_BF16) topk_dispatch<__nv_bfloat16>(L, splits, X, T, a, s);
+  else topk_dispatch<float>(L, splits, X, T, a, s);
   count_launches(1);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// 3b. Fused decode gate (T <= 64, E <= 256): projection + top-K + permute in ONE
+//     launch.  Every CTA computes its projection partials; the last CTA of each
+//     32-token tile (global counter, threadfence pattern) runs top-K / mask for
+//     the tile; the last tile to finish runs the stable permute for all tokens.
+//     Counters live at the start of the zero-initialised workspace and are reset
+//     by their last user, so the kernel is replayable (CUDA graphs).
+// ---------------------------------------------------------------------------
+constexpr int kCounterSlots = 4;  // [0, 2] token tiles, [3] tiles-done
+
+template <typename TX, int NPL>
+__global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ X, const float* __restrict__ nw,
+                                                         const float* __restrict__ W, int T, int d, int d_pad,
+                                                         int kr, float* __restrict__ P, TopkArgs a, int E,
+                                                         int bs, PlanDev p, int* __restrict__ counters) {
+  extern __shared__ float xs[];  // phase 1: token tile; phase 3: permute scratch
+  __shared__ float red_s[8 * kGemvCols * kGemvTT];
+  __shared__ int s_last;
+  const int cols = 2 * a.N;
+  router_gemv_body<TX>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s);
+
+  // ---- last CTA of this token tile: top-K + mask ----
+  __threadfence();
+  __syncthreads();
+  const int tile = blockIdx.z;
+  if (threadIdx.x == 0) s_last = atomicAdd(&counters[tile], 1) == (int)(gridDim.x * gridDim.y) - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int t0 = tile * kGemvTT, nt = min(kGemvTT, T - t0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = t0 + warp; t < t0 + nt; t += 8)
+    topk_token<TX, NPL, kFusedMaxSplit, true>(P, gridDim.y, T, X, t, lane, a);
+  if (threadIdx.x == 0) counters[tile] = 0;
+
+  // ---- last token tile overall: permute all T tokens ----
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&counters[kCounterSlots - 1], 1) == (int)gridDim.z - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  permute_block<int32_t, 8, true>(a.ids32, a.gw, T, a.K + a.S, E, bs, p, reinterpret_cast<int*>(xs));
+  if (threadIdx.x == 0) counters[kCounterSlots - 1] = 0;
+}
+
+bool gate_fused_supported(int T, int N, int E, int d_pad) {
+  return T >= 1 && T <= 64 && N <= 512 && E <= 256 && d_pad % 4 == 0;
+}
+
+template <typename TX, int NPL>
+static cudaError_t fused_launch(dim3 grid, size_t smem, const void* X, const float* nw, const float* W, int T,
+                                int d, int d_pad, int kr, float* P, const TopkArgs& a, int E, int bs,
+                                const PlanDev& p, int* counters, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    set_smem(gate_fused_kernel<TX, NPL>, 160 * 1024);
+    attr = true;
+  }
+  gate_fused_kernel<TX, NPL><<<grid, 256, smem, s>>>((const TX*)X, nw, W, T, d, d_pad, kr, P, a, E, bs, p, counters);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, const float* gate_wT, int T,
+                              int d, int d_pad, float* P, const TopkArgs& a, int E, int bs,
+                              const PlanDev& p, int* counters, cudaStream_t s) {
+  const int cols = 2 * a.N;
+  const int kr = gemv_kr(T, cols, d_pad, kFusedMaxSplit);
+  dim3 grid(ceil_div(cols, 8 * kGemvCols), ceil_div(d_pad, kr), ceil_div(T, kGemvTT));
+  if ((int)grid.y > kFusedMaxSplit || (int)grid.z > kCounterSlots - 1) return cudaErrorInvalidValue;
+  const size_t smem = std::max((size_t)kGemvTT * kr * sizeof(float), (size_t)(8 * E + E + 1 + 32) * sizeof(int));
+  const int npl = ceil_div(a.N, 32);
+  cudaError_t e;
+#define BEAM_FUSED(TX_)                                                                                        \
+  if (npl <= 1) e = fused_launch<TX_, 1>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, p, counters, s); \
+  else if (npl <= 2) e = fused_launch<TX_, 2>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, p, counters, s); \
+  else if (npl <= 4) e = fused_launch<TX_, 4>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, p, counters, s); \
+  else if (npl <= 8) e = fused_launch<TX_, 8>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, p, counters, s); \
+  else e = fused_launch<TX_, 16>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, p, counters, s);
+  if (x_dtype == BEAM_BF16) {
+    BEAM_FUSED(__nv_bfloat16)
+  } else {
+    BEAM_FUSED(float)
+  }
+#undef BEAM_FUSED
+  count_launches(1);
+  return e;
 }
 
 // ---------------------------------------------------------------------------

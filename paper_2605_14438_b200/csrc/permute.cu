@@ -9,113 +9,146 @@
 //                                                 ceil(c/bs)*bs
 //   (paper listing   PAPER.md:772-782: vLLM's moe_align_block_size skipping -1)
 //
-// B200 design: one CTA of 32 warps.  Each warp owns a contiguous chunk of the flat
-// id array; pass 1 builds per-warp histograms in shared memory (integer atomics:
-// order-free), pass 2 turns them into per-(warp, expert) bases with a scan in
-// expert-major / warp-minor order, pass 3 re-walks each chunk in order and ranks
-// equal experts inside a 32-entry step with __match_any_sync.  The result is the
-// reference's order exactly, with no dependence on scheduling.
-#include "beam_common.cuh"
-#include "beam_internal.h"
+// Small inputs: one CTA of 32 warps (permute_block in route_device.cuh).  Large
+// inputs (prefill, T*K > 16384): two grid-wide passes — per-CTA histograms with
+// the last CTA scanning them into per-(CTA, expert) bases, then an ordered
+// scatter that recomputes per-warp bases inside each CTA.  Both give the
+// reference's order exactly, independent of scheduling.
+#include "route_device.cuh"
 
 namespace beam {
 
 constexpr int kPermuteThreads = 1024;
 constexpr int kPermuteWarps = kPermuteThreads / 32;
 
-// Block-wide exclusive scan of one int per thread (1024 threads).
-__device__ __forceinline__ int block_exclusive_scan(int v, int* scratch, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) scratch[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int w = scratch[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
-    }
-    scratch[lane] = w;  // inclusive warp totals
-  }
-  __syncthreads();
-  const int warp_base = warp > 0 ? scratch[warp - 1] : 0;
-  *total = scratch[31];
-  __syncthreads();
-  return warp_base + x - v;
-}
-
 template <typename IdT>
 __global__ void __launch_bounds__(kPermuteThreads, 1)
-    permute_kernel(const IdT* __restrict__ ids, const float* __restrict__ w, int T, int K, int E,
-                   int bs, PlanDev p) {
+    permute_kernel(const IdT* __restrict__ ids, const float* __restrict__ w, int T, int K, int E, int bs,
+                   PlanDev p) {
   extern __shared__ int smem[];
-  int* hist = smem;                        // [kPermuteWarps][E]
-  int* off_s = hist + kPermuteWarps * E;   // [E + 1]
-  int* scratch = off_s + E + 1;            // [32]
+  permute_block<IdT, kPermuteWarps, false>(ids, w, T, K, E, bs, p, smem);
+}
+
+// ---------------------------------------------------------------------------
+// multi-CTA permute
+// ---------------------------------------------------------------------------
+constexpr int kMcThreads = 256;
+constexpr int kMcWarps = kMcThreads / 32;
+constexpr int kMcChunk = 4096;                  // entries per CTA
+constexpr int kMcPerWarp = kMcChunk / kMcWarps;  // 512, multiple of 32
+constexpr long long kSingleCtaMax = 16384;
+
+// per-warp histograms of this CTA's chunk (shared), sh = [kMcWarps][E]
+template <typename IdT>
+__device__ __forceinline__ void chunk_hist(const IdT* __restrict__ ids, int M, int E, int* sh) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int M = T * K;
-
-  for (int i = tid; i < kPermuteWarps * E; i += kPermuteThreads) hist[i] = 0;
+  for (int i = tid; i < kMcWarps * E; i += kMcThreads) sh[i] = 0;
   __syncthreads();
-
-  const int per_warp = ceil_div(ceil_div(M, kPermuteWarps), 32) * 32;
-  const int begin = min(M, warp * per_warp);
-  const int end = min(M, begin + per_warp);
-
-  // pass 1: per-warp histograms
+  const int begin = blockIdx.x * kMcChunk + warp * kMcPerWarp;
+  const int end = min(M, begin + kMcPerWarp);
   for (int i = begin + lane; i < end; i += 32) {
     const long long e = (long long)ids[i];
-    if (e >= 0 && e < E) atomicAdd(&hist[warp * E + (int)e], 1);
+    if (e >= 0 && e < E) atomicAdd(&sh[warp * E + (int)e], 1);
   }
   __syncthreads();
+}
 
-  // pass 2a: per-(warp, expert) exclusive bases, per-expert totals
-  for (int e = tid; e < E; e += kPermuteThreads) {
+// pass 1: hist_g[cta][e] = this CTA's count of expert e; the last CTA converts
+// them to exclusive bases over CTAs and writes counts / offsets / active / meta.
+template <typename IdT>
+__global__ void __launch_bounds__(kMcThreads) permute_hist_kernel(const IdT* __restrict__ ids, int M, int E,
+                                                                  int bs, PlanDev p, int* __restrict__ hist_g,
+                                                                  int* __restrict__ counter) {
+  extern __shared__ int sh[];
+  __shared__ int s_last;
+  __shared__ int scratch[32];
+  __shared__ int carry[3];
+  const int tid = threadIdx.x;
+  chunk_hist<IdT>(ids, M, E, sh);
+  for (int e = tid; e < E; e += kMcThreads) {
+    int c = 0;
+    for (int q = 0; q < kMcWarps; ++q) c += sh[q * E + e];
+    hist_g[(size_t)blockIdx.x * E + e] = c;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int G = gridDim.x;
+  if (tid == 0) carry[0] = carry[1] = carry[2] = 0;
+  __syncthreads();
+  for (int e0 = 0; e0 < E; e0 += kMcThreads) {
+    const int e = e0 + tid;
     int run = 0;
-    for (int q = 0; q < kPermuteWarps; ++q) {
-      const int c = hist[q * E + e];
-      hist[q * E + e] = run;
+    if (e < E) {
+      int q = 0;
+      for (; q + 8 <= G; q += 8) {  // 8 independent loads per round
+        int c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = __ldcg(hist_g + (size_t)(q + u) * E + e);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          hist_g[(size_t)(q + u) * E + e] = run;
+          run += c[u];
+        }
+      }
+      for (; q < G; ++q) {
+        const int c = __ldcg(hist_g + (size_t)q * E + e);
+        hist_g[(size_t)q * E + e] = run;
+        run += c;
+      }
+      p.counts[e] = run;
+    }
+    int tot_pad, tot_act, tot_real;
+    const int ex_pad = block_exclusive_scan<kMcWarps>(e < E ? round_up(run, bs) : 0, scratch, &tot_pad);
+    const int ex_act = block_exclusive_scan<kMcWarps>(e < E && run > 0 ? 1 : 0, scratch, &tot_act);
+    block_exclusive_scan<kMcWarps>(run, scratch, &tot_real);
+    if (e < E) {
+      p.offsets[e] = carry[0] + ex_pad;
+      if (run > 0) p.active[carry[1] + ex_act] = e;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      carry[0] += tot_pad;
+      carry[1] += tot_act;
+      carry[2] += tot_real;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    p.offsets[E] = carry[0];
+    p.meta[0] = carry[1];
+    p.meta[1] = carry[0];
+    p.meta[2] = carry[2];
+    p.meta[3] = 0;
+    *counter = 0;  // replayable
+  }
+}
+
+// pass 2: ordered scatter.  Per-warp bases = offsets[e] + CTA base + earlier warps.
+template <typename IdT>
+__global__ void __launch_bounds__(kMcThreads) permute_scatter_kernel(const IdT* __restrict__ ids,
+                                                                     const float* __restrict__ w, int M, int K,
+                                                                     int E, PlanDev p,
+                                                                     const int* __restrict__ hist_g) {
+  extern __shared__ int sh[];  // [kMcWarps][E] counts, then bases
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  chunk_hist<IdT>(ids, M, E, sh);
+  for (int e = tid; e < E; e += kMcThreads) {
+    int run = p.offsets[e] + hist_g[(size_t)blockIdx.x * E + e];
+    for (int q = 0; q < kMcWarps; ++q) {
+      const int c = sh[q * E + e];
+      sh[q * E + e] = run;
       run += c;
     }
-    p.counts[e] = run;
-    off_s[e] = run;  // temporarily: count
   }
   __syncthreads();
-
-  // pass 2b: padded offsets + active-expert list (E <= 1024: one expert per thread)
-  {
-    const int c = tid < E ? off_s[tid] : 0;
-    const int padded = round_up(c, bs);
-    int tot_pad, tot_act, tot_real;
-    const int ex_pad = block_exclusive_scan(padded, scratch, &tot_pad);
-    const int ex_act = block_exclusive_scan(c > 0 ? 1 : 0, scratch, &tot_act);
-    block_exclusive_scan(c, scratch, &tot_real);
-    __syncthreads();
-    if (tid < E) {
-      off_s[tid] = ex_pad;
-      p.offsets[tid] = ex_pad;
-      if (c > 0) p.active[ex_act] = tid;
-    }
-    if (tid == 0) {
-      off_s[E] = tot_pad;
-      p.offsets[E] = tot_pad;
-      p.meta[0] = tot_act;
-      p.meta[1] = tot_pad;
-      p.meta[2] = tot_real;
-      p.meta[3] = 0;
-    }
-  }
-  __syncthreads();
-
-  // pass 3: stable scatter
-  for (int base = begin; base < end; base += 32) {
-    const int i = base + lane;
+  const int begin = blockIdx.x * kMcChunk + warp * kMcPerWarp;
+  const int end = min(M, begin + kMcPerWarp);
+  for (int b0 = begin; b0 < end; b0 += 32) {
+    const int i = b0 + lane;
     long long e = -1;
     if (i < end) e = (long long)ids[i];
     const bool valid = i < end && e >= 0 && e < E;
@@ -123,7 +156,7 @@ __global__ void __launch_bounds__(kPermuteThreads, 1)
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     const int rank = __popc(peers & ((1u << lane) - 1u));
     if (valid) {
-      const int pos = off_s[e] + hist[warp * E + e] + rank;
+      const int pos = sh[warp * E + e] + rank;
       const int t = i / K;
       p.tok[pos] = t;
       p.slot[pos] = i - t * K;
@@ -135,14 +168,13 @@ __global__ void __launch_bounds__(kPermuteThreads, 1)
       if (p.slot_expert) p.slot_expert[i] = -1;
     }
     __syncwarp();
-    if (valid && rank == 0) hist[warp * E + e] += __popc(peers);
+    if (valid && rank == 0) sh[warp * E + e] += __popc(peers);
     __syncwarp();
   }
-
-  // padding tail of every expert run
-  for (int e = warp; e < E; e += kPermuteWarps) {
-    const int real_end = off_s[e] + p.counts[e];
-    for (int q = real_end + lane; q < off_s[e + 1]; q += 32) {
+  // padding tails (grid-stride over experts)
+  for (int e = blockIdx.x * kMcWarps + warp; e < E; e += gridDim.x * kMcWarps) {
+    const int real_end = p.offsets[e] + p.counts[e];
+    for (int q = real_end + lane; q < p.offsets[e + 1]; q += 32) {
       p.tok[q] = -1;
       p.slot[q] = -1;
       if (p.w) p.w[q] = 0.0f;
@@ -150,25 +182,49 @@ __global__ void __launch_bounds__(kPermuteThreads, 1)
   }
 }
 
+size_t permute_scratch_bytes(int T, int K, int E) {
+  const long long M = (long long)T * K;
+  const long long G = (M + kMcChunk - 1) / kMcChunk;
+  return (size_t)(G * E + 64) * sizeof(int);
+}
+
 template <typename IdT>
-cudaError_t launch_permute(const IdT* ids, const float* w, int T, int K, int E, int bs,
-                           const PlanDev& p, cudaStream_t s) {
+cudaError_t launch_permute(const IdT* ids, const float* w, int T, int K, int E, int bs, const PlanDev& p,
+                           int* scratch, cudaStream_t s) {
   if (E > kPermuteThreads || bs < 1) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)(kPermuteWarps * E + E + 1 + 32) * sizeof(int);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(permute_kernel<IdT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
+  const long long M = (long long)T * K;
+  if (M <= kSingleCtaMax || scratch == nullptr) {
+    const size_t smem = (size_t)(kPermuteWarps * E + E + 1 + 32) * sizeof(int);
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(permute_kernel<IdT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_set = true;
+    }
+    permute_kernel<IdT><<<1, kPermuteThreads, smem, s>>>(ids, w, T, K, E, bs, p);
+    count_launches(1);
+    return cudaGetLastError();
   }
-  permute_kernel<IdT><<<1, kPermuteThreads, smem, s>>>(ids, w, T, K, E, bs, p);
-  count_launches(1);
+  // scratch: [0, 64) ints = counter (zero-initialised, reset by the last CTA), then hist_g
+  int* counter = scratch;
+  int* hist_g = scratch + 64;
+  const int G = (int)((M + kMcChunk - 1) / kMcChunk);
+  const size_t smem = (size_t)kMcWarps * E * sizeof(int);
+  static bool attr_mc = false;
+  if (!attr_mc) {
+    cudaFuncSetAttribute(permute_hist_kernel<IdT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(permute_scatter_kernel<IdT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr_mc = true;
+  }
+  permute_hist_kernel<IdT><<<G, kMcThreads, smem, s>>>(ids, (int)M, E, bs, p, hist_g, counter);
+  permute_scatter_kernel<IdT><<<G, kMcThreads, smem, s>>>(ids, w, (int)M, K, E, p, hist_g);
+  count_launches(2);
   return cudaGetLastError();
 }
 
-template cudaError_t launch_permute<int32_t>(const int32_t*, const float*, int, int, int, int,
-                                             const PlanDev&, cudaStream_t);
-template cudaError_t launch_permute<int64_t>(const int64_t*, const float*, int, int, int, int,
-                                             const PlanDev&, cudaStream_t);
+template cudaError_t launch_permute<int32_t>(const int32_t*, const float*, int, int, int, int, const PlanDev&,
+                                             int*, cudaStream_t);
+template cudaError_t launch_permute<int64_t>(const int64_t*, const float*, int, int, int, int, const PlanDev&,
+                                             int*, cudaStream_t);
 
 // ---------------------------------------------------------------------------
 // grouped_execute plan preparation: routing weight per planned position, the
@@ -176,12 +232,10 @@ template cudaError_t launch_permute<int64_t>(const int64_t*, const float*, int, 
 // (dispatch/__init__.py:143-144 nnz(weights_hat) == real slots, :152-153 no
 // zero-weight planned slot).  slot_pos / slot_expert must be preset to -1.
 // ---------------------------------------------------------------------------
-__global__ void plan_prepare_kernel(const int32_t* __restrict__ counts,
-                                    const int32_t* __restrict__ offsets,
-                                    const int32_t* __restrict__ tokens,
-                                    const int32_t* __restrict__ slots,
-                                    const float* __restrict__ weights_hat, int T, int K, int N,
-                                    PlanDev p, int32_t* __restrict__ flags) {
+__global__ void plan_prepare_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                                    const int32_t* __restrict__ tokens, const int32_t* __restrict__ slots,
+                                    const float* __restrict__ weights_hat, int T, int K, int N, PlanDev p,
+                                    int32_t* __restrict__ flags) {
   const int e = blockIdx.x;
   const int c = counts[e], off = offsets[e];
   for (int q = threadIdx.x; q < c; q += blockDim.x) {
@@ -194,21 +248,19 @@ __global__ void plan_prepare_kernel(const int32_t* __restrict__ counts,
   }
 }
 
-__global__ void nnz_count_kernel(const float* __restrict__ x, long long n,
-                                 const int32_t* __restrict__ meta, int32_t* __restrict__ flags) {
+__global__ void nnz_count_kernel(const float* __restrict__ x, long long n, const int32_t* __restrict__ meta,
+                                 int32_t* __restrict__ flags) {
   int c = 0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     c += x[i] != 0.0f;
   c = __reduce_add_sync(0xffffffffu, c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(&flags[0], c);
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicSub(&flags[0], meta[2]);
 }
 
-cudaError_t launch_plan_prepare(const int32_t* counts, const int32_t* offsets,
-                                const int32_t* tokens, const int32_t* slots, const int32_t* meta,
-                                const float* weights_hat, int T, int K, int N, const PlanDev& p,
-                                int32_t* flags, cudaStream_t s) {
+cudaError_t launch_plan_prepare(const int32_t* counts, const int32_t* offsets, const int32_t* tokens,
+                                const int32_t* slots, const int32_t* meta, const float* weights_hat, int T, int K,
+                                int N, const PlanDev& p, int32_t* flags, cudaStream_t s) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(p.slot_pos, 0xff, (size_t)T * K * sizeof(int32_t), s))) return e;
   if ((e = cudaMemsetAsync(p.slot_expert, 0xff, (size_t)T * K * sizeof(int32_t), s))) return e;

@@ -1,0 +1,294 @@
+// Device building blocks of the routing half: vector loads, the per-token top-K /
+// softmax / mask step, and the block-level stable permute.  Shared by the
+// stand-alone kernels (gate.cu, permute.cu) and the fused decode gate kernel.
+//
+// Reference semantics (/root/reference/pkg/src/beamoe/):
+//   topk_select / topk_route   moe.py:116-137     desc value, ties -> lower id; softmax
+//                                                 over exactly the K kept logits
+//   mask_forward / mask_route  beam.py:68-72, _kernels.pyx:17-34   a >= thr keeps (NaN masked)
+//   group_by_expert / align    _kernels.pyx:37-66, dispatch/__init__.py:89-126
+#pragma once
+
+#include "beam_common.cuh"
+#include "beam_internal.h"
+
+namespace beam {
+
+// 4 consecutive elements (k % 4 == 0) as float4
+template <typename T> __device__ __forceinline__ float4 ld4(const T* p);
+template <> __device__ __forceinline__ float4 ld4<float>(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+template <> __device__ __forceinline__ float4 ld4<__nv_bfloat16>(const __nv_bfloat16* p) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+  return make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                     __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u));
+}
+
+// norm weights at k..k+3 (zero beyond d; NULL -> ones)
+__device__ __forceinline__ float4 ld_norm4(const float* __restrict__ nw, int k, int d) {
+  if (nw == nullptr) return make_float4(1.f, 1.f, 1.f, 1.f);
+  if (k + 3 < d && (d & 3) == 0) return __ldg(reinterpret_cast<const float4*>(nw + k));
+  return make_float4(k < d ? nw[k] : 0.f, k + 1 < d ? nw[k + 1] : 0.f, k + 2 < d ? nw[k + 2] : 0.f,
+                     k + 3 < d ? nw[k + 3] : 0.f);
+}
+
+// Loads of data written earlier in the same kernel by other CTAs go through L2.
+template <bool CG, typename T>
+__device__ __forceinline__ T ld_maybe_cg(const T* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return *p;
+}
+
+
+// One warp, one token.  L = projection partials [splits][T][2N] (router then mask
+// columns), X = the token rows (stride d_pad) for inv_rms.  NPL = ceil(N / 32).
+template <typename TX, int NPL, int MAXSPLIT, bool CG>
+__device__ __forceinline__ void topk_token(const float* __restrict__ L, int splits, int T,
+                                           const TX* __restrict__ X, int t, int lane,
+                                           const TopkArgs& a) {
+  const int N = a.N, K = a.K, Keff = a.K + a.S;
+  float inv = 1.0f;
+  if (a.has_norm) {  // tensor.py:485-487: (mean(x^2) + eps)^-1/2 over the real d entries
+    const TX* row = X + (size_t)t * a.d_pad;
+    float ss = 0.0f;
+#pragma unroll 8
+    for (int k = 4 * lane; k < a.d_pad; k += 128) {
+      const float4 x = ld4<TX>(row + k);
+      ss = fmaf(x.x, x.x, ss);
+      ss = fmaf(x.y, x.y, ss);
+      ss = fmaf(x.z, x.z, ss);
+      ss = fmaf(x.w, x.w, ss);
+    }
+    ss = warp_sum(ss);
+    inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
+  }
+  if (a.inv_out && lane == 0) a.inv_out[t] = inv;
+
+  // router logits v / mask pre-activations av of this lane's experts j = lane + 32 i,
+  // summed over the split-K partials in split order (all loads issued together)
+  float v[NPL], av[NPL];
+  int rank[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    v[i] = 0.0f;
+    av[i] = 0.0f;
+    rank[i] = -1;
+  }
+#pragma unroll
+  for (int sp = 0; sp < MAXSPLIT; ++sp) {
+    if (sp < splits) {
+      const float* row = L + ((size_t)sp * T + t) * 2 * N;
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) {
+        const int j = lane + 32 * i;
+        if (j < N) {
+          v[i] += ld_maybe_cg<CG>(row + j);
+          av[i] += ld_maybe_cg<CG>(row + N + j);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    v[i] *= inv;
+    av[i] *= inv;
+  }
+
+  float top_val = 0.0f;
+  for (int r = 0; r < K; ++r) {
+    bool have = false;
+    float bv = 0.0f;
+    int bj = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int j = lane + 32 * i;
+      if (j < N && rank[i] < 0 && (!have || v[i] > bv)) {  // ascending j in a lane: ties keep the lower j
+        have = true;
+        bv = v[i];
+        bj = j;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      const bool ohave = __shfl_xor_sync(0xffffffffu, (int)have, o) != 0;
+      if (ohave && (!have || ov > bv || (ov == bv && oj < bj))) {
+        bv = ov;
+        bj = oj;
+        have = true;
+      }
+    }
+    if (r == 0) top_val = bv;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i)
+      if (lane + 32 * i == bj) rank[i] = r;
+  }
+
+  // softmax over the K kept logits (tensor.py:440-451): exp(l - max) / sum
+  float part = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i)
+    if (rank[i] >= 0) part += expf(v[i] - top_val);
+  const float denom = warp_sum(part);
+
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    if (j >= N) continue;
+    const float x = av[i];
+    const bool keep = x >= a.thr;  // NaN -> false
+    const float g = rank[i] >= 0 ? expf(v[i] - top_val) / denom : 0.0f;
+    if (rank[i] >= 0) {
+      const int r = rank[i];
+      const size_t o = (size_t)t * Keff + r;
+      a.ids32[o] = keep ? j : -1;
+      a.gw[o] = keep ? g : 0.0f;
+      if (a.topk_ids) a.topk_ids[(size_t)t * K + r] = j;
+      if (a.masked_ids) a.masked_ids[(size_t)t * K + r] = keep ? j : -1;
+    }
+    const size_t od = (size_t)t * N + j;
+    if (a.logits) a.logits[od] = v[i];
+    if (a.weights) a.weights[od] = g;
+    if (a.pre_act) a.pre_act[od] = x;
+    if (a.raw_mask) a.raw_mask[od] = sigmoid_ref(x);
+    if (a.mask) a.mask[od] = keep ? 1.0f : 0.0f;
+  }
+  // shared experts: always-on slots K..K+S-1, weight 1.0 (beam.py:163-164)
+  for (int s = lane; s < a.S; s += 32) {
+    const size_t o = (size_t)t * Keff + K + s;
+    a.ids32[o] = N + s;
+    a.gw[o] = 1.0f;
+  }
+}
+
+// Block-wide exclusive scan of one int per thread (NW warps, NW <= 32).
+template <int NW>
+__device__ __forceinline__ int block_exclusive_scan(int v, int* scratch, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < NW ? scratch[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    scratch[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  const int warp_base = warp > 0 ? scratch[warp - 1] : 0;
+  *total = scratch[NW - 1];
+  __syncthreads();
+  return warp_base + x - v;
+}
+
+// Stable counting sort of the surviving (t, k) entries by expert, one CTA of NW
+// warps (E <= 32 * NW).  Each warp owns a contiguous chunk of the flat id array;
+// per-warp histograms (integer shared atomics: order-free) -> per-(warp, expert)
+// bases (expert-major / warp-minor scan) -> ordered re-walk ranking equal experts
+// inside each 32-entry step with __match_any_sync.  Identical to the reference's
+// order (ascending flat index inside an expert) whatever the scheduling.
+// smem: NW*E + E + 1 + 32 ints.
+template <typename IdT, int NW, bool CG>
+__device__ __forceinline__ void permute_block(const IdT* __restrict__ ids, const float* __restrict__ w,
+                                              int T, int K, int E, int bs, const PlanDev& p, int* smem) {
+  int* hist = smem;                 // [NW][E]
+  int* off_s = hist + NW * E;       // [E + 1]
+  int* scratch = off_s + E + 1;     // [32]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int M = T * K;
+
+  for (int i = tid; i < NW * E; i += NW * 32) hist[i] = 0;
+  __syncthreads();
+
+  const int per_warp = ceil_div(ceil_div(M, NW), 32) * 32;
+  const int begin = min(M, warp * per_warp);
+  const int end = min(M, begin + per_warp);
+
+  for (int i = begin + lane; i < end; i += 32) {
+    const long long e = (long long)ld_maybe_cg<CG>(ids + i);
+    if (e >= 0 && e < E) atomicAdd(&hist[warp * E + (int)e], 1);
+  }
+  __syncthreads();
+
+  for (int e = tid; e < E; e += NW * 32) {
+    int run = 0;
+    for (int q = 0; q < NW; ++q) {
+      const int c = hist[q * E + e];
+      hist[q * E + e] = run;
+      run += c;
+    }
+    p.counts[e] = run;
+    off_s[e] = run;  // temporarily: count
+  }
+  __syncthreads();
+
+  {
+    const int c = tid < E ? off_s[tid] : 0;
+    const int padded = round_up(c, bs);
+    int tot_pad, tot_act, tot_real;
+    const int ex_pad = block_exclusive_scan<NW>(padded, scratch, &tot_pad);
+    const int ex_act = block_exclusive_scan<NW>(c > 0 ? 1 : 0, scratch, &tot_act);
+    block_exclusive_scan<NW>(c, scratch, &tot_real);
+    __syncthreads();
+    if (tid < E) {
+      off_s[tid] = ex_pad;
+      p.offsets[tid] = ex_pad;
+      if (c > 0) p.active[ex_act] = tid;
+    }
+    if (tid == 0) {
+      off_s[E] = tot_pad;
+      p.offsets[E] = tot_pad;
+      p.meta[0] = tot_act;
+      p.meta[1] = tot_pad;
+      p.meta[2] = tot_real;
+      p.meta[3] = 0;
+    }
+  }
+  __syncthreads();
+
+  for (int base = begin; base < end; base += 32) {
+    const int i = base + lane;
+    long long e = -1;
+    if (i < end) e = (long long)ld_maybe_cg<CG>(ids + i);
+    const bool valid = i < end && e >= 0 && e < E;
+    const int key = valid ? (int)e : (E + lane);
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (valid) {
+      const int pos = off_s[e] + hist[warp * E + e] + rank;
+      const int t = i / K;
+      p.tok[pos] = t;
+      p.slot[pos] = i - t * K;
+      if (p.w) p.w[pos] = w ? ld_maybe_cg<CG>(w + i) : 0.0f;
+      if (p.slot_pos) p.slot_pos[i] = pos;
+      if (p.slot_expert) p.slot_expert[i] = (int)e;
+    } else if (i < end) {
+      if (p.slot_pos) p.slot_pos[i] = -1;
+      if (p.slot_expert) p.slot_expert[i] = -1;
+    }
+    __syncwarp();
+    if (valid && rank == 0) hist[warp * E + e] += __popc(peers);
+    __syncwarp();
+  }
+
+  for (int e = warp; e < E; e += NW) {
+    const int real_end = off_s[e] + p.counts[e];
+    for (int q = real_end + lane; q < off_s[e + 1]; q += 32) {
+      p.tok[q] = -1;
+      p.slot[q] = -1;
+      if (p.w) p.w[q] = 0.0f;
+    }
+  }
+}
+
+}  // namespace beam
