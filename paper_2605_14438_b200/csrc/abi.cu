@@ -78,6 +78,7 @@ struct LayerWs {
   int cap;
   int* counters;   // [64] grid-completion counters (zero-initialised workspace; reset after use)
   int* pscratch;   // multi-CTA permute scratch (its first 64 ints are a counter)
+  void* rscratch;  // prefill tensor-core router: bf16 3-way split of the gate weights
   void* xperm;     // [cap, d_pad] bf16 x_n in plan order (tc path)
   void* act16;     // [cap, f_pad] bf16 (tc path)
   void* xpad;      // [T, d_pad] input rows re-strided (only when d_h % 8 != 0)
@@ -101,13 +102,14 @@ static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, La
   LayerWs w;
   w.counters = c.take<int>(64);
   w.pscratch = c.take<int>(permute_scratch_bytes(T, Krow, g.E) / sizeof(int));
+  w.rscratch = T > 64 ? c.take<char>(router_tc_scratch_bytes(2 * g.N, g.d_pad)) : nullptr;
   w.tc = use_tc(L, g, T, Krow);
   w.cap = (int)cap;
   w.xperm = w.tc ? c.take<__nv_bfloat16>(cap * g.d_pad) : nullptr;
   w.act16 = w.tc ? c.take<__nv_bfloat16>(cap * g.f_pad) : nullptr;
   w.xpad = g.d != g.d_pad ? c.take<float>((size_t)T * g.d_pad) : nullptr;
   w.inv = c.take<float>((size_t)T);
-  w.logits2 = c.take<float>((size_t)router_splits(T, 2 * g.N, g.d_pad) * T * 2 * g.N);
+  w.logits2 = c.take<float>((size_t)(T <= 64 ? 16 : 1) * T * 2 * g.N);  // split-K partials (<= 16 splits)
   w.ids32 = c.take<int32_t>(M);
   w.gw = c.take<float>(M);
   w.plan.counts = c.take<int32_t>(g.E);
@@ -194,7 +196,11 @@ static TopkArgs topk_args(const beam_layer_t& L, const Dims& g, const beam_outpu
 static cudaError_t run_gate(const beam_layer_t& L, const Dims& g, const void* X, int h_dtype, int T,
                             const beam_outputs_t* o, LayerWs& w, cudaStream_t s) {
   const float* nw = L.has_norm ? L.norm_w : nullptr;
-  cudaError_t e = launch_router(X, h_dtype, nw, L.gate_wT, T, 2 * g.N, g.d, g.d_pad, w.logits2, s);
+  cudaError_t e;
+  if (w.rscratch && router_tc_supported(T, 2 * g.N, g.d_pad, h_dtype))
+    e = launch_router_tc(X, nw, L.gate_wT, T, 2 * g.N, g.d, g.d_pad, w.logits2, w.rscratch, s);
+  else
+    e = launch_router(X, h_dtype, nw, L.gate_wT, T, 2 * g.N, g.d, g.d_pad, w.logits2, s);
   if (e != cudaSuccess) return e;
   return launch_topk_mask(w.logits2, router_splits(T, 2 * g.N, g.d_pad), X, h_dtype, T, topk_args(L, g, o, w), s);
 }

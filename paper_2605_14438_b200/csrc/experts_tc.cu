@@ -43,10 +43,11 @@ constexpr int kThreads = 192;
 constexpr int kMaxE = 1024;
 
 struct Args {
-  int mode;  // 0 gate/up, 1 down
+  int mode;  // 0 gate/up, 1 down, 2 router projection (fp32 out, no weight)
   int E;
   int m_rows;  // A rows per expert
   int K;
+  int b_kblocks;  // B k-blocks before the coordinate wraps (router: 3 bf16 splits of W share one h)
   const int32_t* counts;
   const int32_t* offsets;
   const float* w;
@@ -237,7 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(&full[stage], kABytes + nbox * kBBoxBytes);
           tma_load_2d(sa + stage * kABytes, &tmA, &full[stage], kb * BK, tl.a_row0);
           for (int c = 0; c < nbox; ++c)
-            tma_load_2d(sb + stage * kBBytes + c * kBBoxBytes, &tmB, &full[stage], kb * BK, tl.b_row0 + c * kBBox);
+            tma_load_2d(sb + stage * kBBytes + c * kBBoxBytes, &tmB, &full[stage], (kb % args.b_kblocks) * BK,
+                        tl.b_row0 + c * kBBox);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (col < tl.ntok)
               args.act[(size_t)(tl.b_row0 + col) * args.f_pad + f] = __float2bfloat16_rn(activation<BEAM_ACT_SILU>(g) * u);
           }
-        } else {
+        } else if (args.mode == 1) {
           const int row = tl.m_tile * BM + lane_base + lane;  // output channel
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -315,6 +317,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int pos = tl.b_row0 + col;
               args.opair[(size_t)pos * args.d_pad + row] = v[j] * __ldg(args.w + pos);
             }
+          }
+        } else {
+          const int row = tl.m_tile * BM + lane_base + lane;  // router / mask column
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = c0 + j;
+            if (col < tl.ntok) args.opair[(size_t)(tl.b_row0 + col) * args.m_rows + row] = v[j];
           }
         }
       }
@@ -337,10 +346,14 @@ template <typename TX>
 __global__ void __launch_bounds__(256) pack_x_kernel(const TX* __restrict__ h, const float* __restrict__ inv,
                                                      const float* __restrict__ nw, int d, int d_pad,
                                                      PlanDev p, int cap, __nv_bfloat16* __restrict__ X) {
+  extern __shared__ float nws[];  // norm weights (zero-padded to d_pad), shared by all rows
+  for (int k = threadIdx.x; k < d_pad; k += blockDim.x) nws[k] = nw ? (k < d ? nw[k] : 0.0f) : 1.0f;
+  __syncthreads();
   const int total = p.meta[1];
+  const int lane = threadIdx.x & 31;
+  constexpr int kU = 8;  // 16-byte stripes per lane in flight
   for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < min(total, cap); row += gridDim.x * 8) {
     const int tok = p.tok[row];
-    const int lane = threadIdx.x & 31;
     __nv_bfloat16* dst = X + (size_t)row * d_pad;
     if (tok < 0) {
       for (int k = lane * 8; k < d_pad; k += 256) *reinterpret_cast<uint4*>(dst + k) = make_uint4(0, 0, 0, 0);
@@ -348,27 +361,36 @@ __global__ void __launch_bounds__(256) pack_x_kernel(const TX* __restrict__ h, c
     }
     const float s = inv ? inv[tok] : 1.0f;
     const TX* src = h + (size_t)tok * d_pad;
-    for (int k = lane * 8; k < d_pad; k += 256) {
-      float x[8];
-      if constexpr (sizeof(TX) == 2) {
-        unpack<__nv_bfloat16>(ld_cached(src + k), x);
-      } else {
-        unpack<float>(ld_cached(src + k), x);
-        unpack<float>(ld_cached(src + k + 4), x + 4);
-      }
-      uint32_t o[4];
+    for (int k0 = lane * 8; k0 < d_pad; k0 += 256 * kU) {
+      float x[kU][8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float a = x[2 * q], b = x[2 * q + 1];
-        if (nw) {
-          const int k0 = k + 2 * q;
-          a = (a * s) * (k0 < d ? __ldg(nw + k0) : 0.0f);
-          b = (b * s) * (k0 + 1 < d ? __ldg(nw + k0 + 1) : 0.0f);
+      for (int u = 0; u < kU; ++u) {  // all loads first
+        const int k = k0 + 256 * u;
+        if (k < d_pad) {
+          if constexpr (sizeof(TX) == 2) {
+            unpack<__nv_bfloat16>(ld_cached(src + k), x[u]);
+          } else {
+            unpack<float>(ld_cached(src + k), x[u]);
+            unpack<float>(ld_cached(src + k + 4), x[u] + 4);
+          }
         }
-        const __nv_bfloat162 v2 = __floats2bfloat162_rn(a, b);
-        o[q] = *reinterpret_cast<const uint32_t*>(&v2);
       }
-      *reinterpret_cast<uint4*>(dst + k) = make_uint4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int k = k0 + 256 * u;
+        if (k < d_pad) {
+          uint32_t o[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            // x_n = (x * inv_rms) * w (tensor.py:487)
+            const float a = (x[u][2 * q] * s) * nws[k + 2 * q];
+            const float b = (x[u][2 * q + 1] * s) * nws[k + 2 * q + 1];
+            const __nv_bfloat162 v2 = __floats2bfloat162_rn(a, b);
+            o[q] = *reinterpret_cast<const uint32_t*>(&v2);
+          }
+          *reinterpret_cast<uint4*>(dst + k) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      }
     }
   }
 }
@@ -419,9 +441,9 @@ cudaError_t launch_pack_x(const void* h, int h_dtype, const float* inv, const fl
                           const PlanDev& p, int cap, void* xperm, cudaStream_t s) {
   const int grid = std::max(1, std::min(num_sms() * 8, (cap + 7) / 8));
   if (h_dtype == BEAM_BF16)
-    tc::pack_x_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
+    tc::pack_x_kernel<__nv_bfloat16><<<grid, 256, g.d_pad * sizeof(float), s>>>((const __nv_bfloat16*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
   else
-    tc::pack_x_kernel<float><<<grid, 256, 0, s>>>((const float*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
+    tc::pack_x_kernel<float><<<grid, 256, g.d_pad * sizeof(float), s>>>((const float*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -441,13 +463,71 @@ cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* 
     cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(kMaxE));
     attr = true;
   }
-  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
+  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
   grouped_gemm_kernel<<<num_sms(), kThreads, smem, s>>>(mA1, mB1, a1);
   count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  Args a2{1, g.E, g.d_pad, g.f_pad, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
+  Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
   grouped_gemm_kernel<<<num_sms(), kThreads, smem, s>>>(mA2, mB2, a2);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Prefill router / mask-router projection on the tensor cores.
+// logits = h . (w_norm o W)^T with h bf16 (exact) and W split into three bf16
+// terms W ~= hi + mid + lo (24 significant bits): the three products are exact
+// in fp32 and accumulate in fp32 in TMEM, i.e. fp32-accurate routing at
+// bf16 tensor-core speed.  The splits are laid side by side along K (A row c =
+// [hi | mid | lo]); B (= h) wraps every d_pad/64 k-blocks, so one GEMM of
+// K = 3 d_pad produces the sum.
+// ---------------------------------------------------------------------------
+__global__ void split_router_kernel(const float* __restrict__ W, const float* __restrict__ nw, int cols, int d,
+                                    int d_pad, __nv_bfloat16* __restrict__ A3, int T, int32_t* __restrict__ plan1) {
+  const size_t n = (size_t)cols * d_pad;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / d_pad), k = (int)(i % d_pad);
+    const float w = W[i] * (nw ? (k < d ? nw[k] : 0.0f) : 1.0f);
+    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+    const float r1 = w - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+    __nv_bfloat16* row = A3 + (size_t)c * 3 * d_pad;
+    row[k] = hi;
+    row[d_pad + k] = mid;
+    row[2 * d_pad + k] = lo;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    plan1[0] = T;  // counts[0]
+    plan1[1] = 0;  // offsets[0]
+  }
+}
+
+bool router_tc_supported(int T, int cols, int d_pad, int x_dtype) {
+  return T > 64 && x_dtype == BEAM_BF16 && cols % tc::BM == 0 && d_pad % tc::BK == 0;
+}
+
+size_t router_tc_scratch_bytes(int cols, int d_pad) { return (size_t)cols * 3 * d_pad * 2 + 256; }
+
+cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* gate_wT, int T, int cols, int d,
+                             int d_pad, float* P, void* scratch, cudaStream_t s) {
+  using namespace tc;
+  __nv_bfloat16* A3 = reinterpret_cast<__nv_bfloat16*>(scratch);
+  int32_t* plan1 = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(scratch) + (size_t)cols * 3 * d_pad * 2);
+  split_router_kernel<<<std::min(4096, (int)(((size_t)cols * d_pad + 255) / 256)), 256, 0, s>>>(
+      gate_wT, norm_w, cols, d, d_pad, A3, T, plan1);
+  count_launches(1);
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, A3, (uint64_t)cols, 3ull * d_pad, BM) || !make_map(&mB, X, (uint64_t)T, d_pad, kBBox))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(kMaxE));
+    attr = true;
+  }
+  Args a{2, 1, cols, 3 * d_pad, d_pad / BK, plan1, plan1 + 1, nullptr, nullptr, 0, P, 0};
+  grouped_gemm_kernel<<<num_sms(), kThreads, smem_bytes(1), s>>>(mA, mB, a);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -170,7 +170,7 @@ constexpr int kGemvK = 128;      // k elements per lane-row step (32 lanes x 4)
 constexpr int kGemvSteps = 8;    // kr <= 1024
 constexpr int kFusedMaxSplit = 4;
 
-template <typename TX>
+template <typename TX, int TT>
 __device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const float* __restrict__ nw,
                                                  const float* __restrict__ W, int T, int cols, int d,
                                                  int d_pad, int kr, float* __restrict__ P, float* xs,
@@ -178,8 +178,8 @@ __device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int c0 = (blockIdx.x * 8 + wib) * kGemvCols;
   const int split = blockIdx.y;
-  const int t0 = blockIdx.z * kGemvTT;
-  const int nt = min(kGemvTT, T - t0);
+  const int t0 = blockIdx.z * TT;
+  const int nt = min(TT, T - t0);
   const int ks = split * kr, ke = min(d_pad, ks + kr);
   const int kn = ke - ks;
   for (int v = threadIdx.x; v < nt * (kn >> 2); v += 256) {
@@ -201,32 +201,32 @@ __device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const
     }
   }
   __syncthreads();
-  float acc[kGemvCols * kGemvTT];
+  float acc[kGemvCols * TT];
 #pragma unroll
-  for (int i = 0; i < kGemvCols * kGemvTT; ++i) acc[i] = 0.0f;
+  for (int i = 0; i < kGemvCols * TT; ++i) acc[i] = 0.0f;
 #pragma unroll
   for (int i = 0; i < kGemvSteps; ++i) {
     const int kk = 4 * lane + kGemvK * i;
     if (ks + kk < ke) {
       const float4 a = wa[i], b = wb[i];
 #pragma unroll
-      for (int t = 0; t < kGemvTT; ++t) {
+      for (int t = 0; t < TT; ++t) {
         if (t < nt) {
           const float4 x = *reinterpret_cast<const float4*>(xs + t * kr + kk);
-          float s0 = acc[t], s1 = acc[kGemvTT + t];
+          float s0 = acc[t], s1 = acc[TT + t];
           s0 = fmaf(a.x, x.x, s0); s0 = fmaf(a.y, x.y, s0); s0 = fmaf(a.z, x.z, s0); s0 = fmaf(a.w, x.w, s0);
           s1 = fmaf(b.x, x.x, s1); s1 = fmaf(b.y, x.y, s1); s1 = fmaf(b.z, x.z, s1); s1 = fmaf(b.w, x.w, s1);
           acc[t] = s0;
-          acc[kGemvTT + t] = s1;
+          acc[TT + t] = s1;
         }
       }
     }
   }
-  warp_reduce_to_smem<kGemvCols * kGemvTT>(acc, red_s + wib * kGemvCols * kGemvTT, lane);
+  warp_reduce_to_smem<kGemvCols * TT>(acc, red_s + wib * kGemvCols * TT, lane);
   if (c0 < cols) {
-    for (int i = lane; i < kGemvCols * kGemvTT; i += 32) {
-      const int j = i / kGemvTT, t = i % kGemvTT;
-      if (t < nt && c0 + j < cols) P[((size_t)split * T + t0 + t) * cols + c0 + j] = red_s[wib * kGemvCols * kGemvTT + i];
+    for (int i = lane; i < kGemvCols * TT; i += 32) {
+      const int j = i / TT, t = i % TT;
+      if (t < nt && c0 + j < cols) P[((size_t)split * T + t0 + t) * cols + c0 + j] = red_s[wib * kGemvCols * TT + i];
     }
   }
 }
@@ -239,13 +239,13 @@ __global__ void __launch_bounds__(256) router_gemv_kernel(const TX* __restrict__
                                                           float* __restrict__ P) {
   extern __shared__ float xs[];
   __shared__ float red_s[8 * kGemvCols * kGemvTT];
-  router_gemv_body<TX>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s);
+  router_gemv_body<TX, kGemvTT>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s);
 }
 
 // k-range per split: enough CTAs to cover the SMs, kr <= kGemvSteps * 128
-static int gemv_kr(int T, int cols, int d_pad, int max_split) {
+static int gemv_kr(int T, int cols, int d_pad, int max_split, int tt = kGemvTT) {
   const int col_ctas = ceil_div(cols, 8 * kGemvCols);
-  const int tok_ctas = ceil_div(T, kGemvTT);
+  const int tok_ctas = ceil_div(T, tt);
   int s = ceil_div(num_sms(), col_ctas * tok_ctas);
   const int smin = ceil_div(d_pad, kGemvSteps * kGemvK);
   s = std::min(s, max_split);
@@ -332,7 +332,8 @@ cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dt
 //     Counters live at the start of the zero-initialised workspace and are reset
 //     by their last user, so the kernel is replayable (CUDA graphs).
 // ---------------------------------------------------------------------------
-constexpr int kCounterSlots = 4;  // [0, 2] token tiles, [3] tiles-done
+constexpr int kFusedTT = 8;        // tokens per fused-gate tile (one warp per token in phase 2)
+constexpr int kCounterSlots = 16;  // [0, 8) token tiles, [15] tiles-done
 
 template <typename TX, int NPL>
 __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ X, const float* __restrict__ nw,
@@ -340,10 +341,10 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
                                                          int kr, float* __restrict__ P, TopkArgs a, int E,
                                                          int bs, PlanDev p, int* __restrict__ counters) {
   extern __shared__ float xs[];  // phase 1: token tile; phase 3: permute scratch
-  __shared__ float red_s[8 * kGemvCols * kGemvTT];
+  __shared__ float red_s[8 * kGemvCols * kFusedTT];
   __shared__ int s_last;
   const int cols = 2 * a.N;
-  router_gemv_body<TX>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s);
+  router_gemv_body<TX, kFusedTT>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s);
 
   // ---- last CTA of this token tile: top-K + mask ----
   __threadfence();
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int t0 = tile * kGemvTT, nt = min(kGemvTT, T - t0);
+  const int t0 = tile * kFusedTT, nt = min(kFusedTT, T - t0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int t = t0 + warp; t < t0 + nt; t += 8)
     topk_token<TX, NPL, kFusedMaxSplit, true>(P, gridDim.y, T, X, t, lane, a);
@@ -391,10 +392,10 @@ cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, c
                               int d, int d_pad, float* P, const TopkArgs& a, int E, int bs,
                               const PlanDev& p, int* counters, cudaStream_t s) {
   const int cols = 2 * a.N;
-  const int kr = gemv_kr(T, cols, d_pad, kFusedMaxSplit);
-  dim3 grid(ceil_div(cols, 8 * kGemvCols), ceil_div(d_pad, kr), ceil_div(T, kGemvTT));
+  const int kr = gemv_kr(T, cols, d_pad, kFusedMaxSplit, kFusedTT);
+  dim3 grid(ceil_div(cols, 8 * kGemvCols), ceil_div(d_pad, kr), ceil_div(T, kFusedTT));
   if ((int)grid.y > kFusedMaxSplit || (int)grid.z > kCounterSlots - 1) return cudaErrorInvalidValue;
-  const size_t smem = std::max((size_t)kGemvTT * kr * sizeof(float), (size_t)(8 * E + E + 1 + 32) * sizeof(int));
+  const size_t smem = std::max((size_t)kFusedTT * kr * sizeof(float), (size_t)(8 * E + E + 1 + 32) * sizeof(int));
   const int npl = ceil_div(a.N, 32);
   cudaError_t e;
 #define BEAM_FUSED(TX_)                                                                                        \
