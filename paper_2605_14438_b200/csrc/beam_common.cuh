@@ -81,6 +81,15 @@ template <> __device__ __forceinline__ float from_f32<float>(float v) { return v
 template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
 // ---------------------------------------------------------------------------
+// programmatic dependent launch (PDL): kernels of the layer chain are launched
+// with programmatic stream serialization, so a kernel's launch and prologue
+// overlap its predecessor's tail; griddep_wait() blocks until the predecessor
+// grid has completed and its memory is visible (no-op without PDL).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
 // warp reductions
 // ---------------------------------------------------------------------------
 

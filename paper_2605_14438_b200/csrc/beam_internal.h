@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/beam_b200.h"
 
 namespace beam {
@@ -56,6 +58,25 @@ struct TopkArgs {
 
 int num_sms();
 cudaError_t record(cudaError_t e);
+
+// Launch with programmatic stream serialization (PDL) so the kernel's launch and
+// prologue overlap the previous kernel on the stream.  Kernels launched this way
+// call griddep_wait() before reading their predecessor's outputs.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 void count_launches(int n);  // bookkeeping for beam_kernel_launches()
 
 // gate.cu

@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
   int* ps = sm + Keff;       // [Keff]
   int* sorted = sm + 2 * Keff;  // [Keff]
   __shared__ int nvalid_s;
+  griddep_wait();
   const int t = blockIdx.x;
   for (int k = threadIdx.x; k < Keff; k += blockDim.x) {
     const int pos = slot_pos[(size_t)t * Keff + k];
@@ -82,13 +83,13 @@ cudaError_t launch_combine(const PlanDev& p, const float* opair, int T, int Keff
   if (T <= 0) return cudaSuccess;
   const size_t smem = (size_t)3 * Keff * sizeof(int);
   if (out_dtype == BEAM_F32 && h_dtype == BEAM_F32)
-    combine_kernel<float, float><<<T, 256, smem, s>>>(p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const float*)h, (float*)out);
+    launch_pdl(combine_kernel<float, float>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const float*)h, (float*)out);
   else if (out_dtype == BEAM_BF16 && h_dtype == BEAM_BF16)
-    combine_kernel<__nv_bfloat16, __nv_bfloat16><<<T, 256, smem, s>>>(p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const __nv_bfloat16*)h, (__nv_bfloat16*)out);
+    launch_pdl(combine_kernel<__nv_bfloat16, __nv_bfloat16>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const __nv_bfloat16*)h, (__nv_bfloat16*)out);
   else if (out_dtype == BEAM_F32 && h_dtype == BEAM_BF16)
-    combine_kernel<__nv_bfloat16, float><<<T, 256, smem, s>>>(p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const __nv_bfloat16*)h, (float*)out);
+    launch_pdl(combine_kernel<__nv_bfloat16, float>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const __nv_bfloat16*)h, (float*)out);
   else
-    combine_kernel<float, __nv_bfloat16><<<T, 256, smem, s>>>(p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const float*)h, (__nv_bfloat16*)out);
+    launch_pdl(combine_kernel<float, __nv_bfloat16>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const float*)h, (__nv_bfloat16*)out);
   count_launches(1);
   return cudaGetLastError();
 }

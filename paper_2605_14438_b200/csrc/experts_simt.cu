@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_cta_kernel(const TW* __res
                                                              float* __restrict__ act) {
   __shared__ float part[kWarps * 32];
   __shared__ float red[32];
+  griddep_wait();
   const int groups = f_pad / 4;
   const long long total = (long long)p.meta[0] * groups;
   for (long long item = blockIdx.x; item < total; item += gridDim.x) {
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, 2) down_cta_kernel(const TW* __restr
                                                            float* __restrict__ opair) {
   __shared__ float part[kWarps * 32];
   __shared__ float red[64];
+  griddep_wait();
   const int groups = ceil_div(d_pad, 16);
   const long long total = (long long)p.meta[0] * groups;
   for (long long item = blockIdx.x; item < total; item += gridDim.x) {
@@ -315,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_warp_kernel(const TW* __re
   __shared__ float red_s[kWarps][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * kWarps + wib, nwarps = gridDim.x * kWarps;
+  griddep_wait();
   const int groups = f_pad / 4;
   const long long total = (long long)p.meta[0] * groups;
   for (long long item = gwarp; item < total; item += nwarps) {
@@ -398,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, 2) down_warp_kernel(const TW* __rest
   __shared__ float red_s[kWarps][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * kWarps + wib, nwarps = gridDim.x * kWarps;
+  griddep_wait();
   const int groups = d_pad / 8;
   const long long total = (long long)p.meta[0] * groups;
   for (long long item = gwarp; item < total; item += nwarps) {
@@ -433,14 +437,14 @@ static void gateup_dispatch(const beam_layer_t& L, const Dims& g, const void* X,
                             cudaStream_t s) {
   if (cta) {
     if (L.activation == BEAM_ACT_SILU)
-      gateup_cta_kernel<TW, TX, BEAM_ACT_SILU><<<grid, kThreads, 0, s>>>((const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+      launch_pdl(gateup_cta_kernel<TW, TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, (const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
     else
-      gateup_cta_kernel<TW, TX, BEAM_ACT_IDENTITY><<<grid, kThreads, 0, s>>>((const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+      launch_pdl(gateup_cta_kernel<TW, TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, (const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
   } else {
     if (L.activation == BEAM_ACT_SILU)
-      gateup_warp_kernel<TW, TX, BEAM_ACT_SILU><<<grid, kThreads, 0, s>>>((const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+      launch_pdl(gateup_warp_kernel<TW, TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, (const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
     else
-      gateup_warp_kernel<TW, TX, BEAM_ACT_IDENTITY><<<grid, kThreads, 0, s>>>((const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+      launch_pdl(gateup_warp_kernel<TW, TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, (const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
   }
 }
 
@@ -471,11 +475,11 @@ cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const 
   const int grid = num_sms() * 2;
   const bool cta = small_batch(T);
   if (L.wdtype == BEAM_BF16) {
-    if (cta) down_cta_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>((const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
-    else down_warp_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>((const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+    if (cta) launch_pdl(down_cta_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+    else launch_pdl(down_warp_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
   } else {
-    if (cta) down_cta_kernel<float><<<grid, kThreads, 0, s>>>((const float*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
-    else down_warp_kernel<float><<<grid, kThreads, 0, s>>>((const float*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+    if (cta) launch_pdl(down_cta_kernel<float>, grid, kThreads, 0, s, (const float*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+    else launch_pdl(down_warp_kernel<float>, grid, kThreads, 0, s, (const float*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
   }
   count_launches(1);
   return cudaGetLastError();

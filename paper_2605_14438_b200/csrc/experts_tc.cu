@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* tile_off = reinterpret_cast<int*>(tmem_slot + 4);  // [E + 1]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  griddep_wait();  // PDL: the plan / operands come from the previous kernel
   const int E = args.E;
   const int MT = args.m_rows / BM;
   const int KB = args.K / BK;
@@ -349,6 +350,7 @@ __global__ void __launch_bounds__(256) pack_x_kernel(const TX* __restrict__ h, c
   extern __shared__ float nws[];  // norm weights (zero-padded to d_pad), shared by all rows
   for (int k = threadIdx.x; k < d_pad; k += blockDim.x) nws[k] = nw ? (k < d ? nw[k] : 0.0f) : 1.0f;
   __syncthreads();
+  griddep_wait();
   const int total = p.meta[1];
   const int lane = threadIdx.x & 31;
   constexpr int kU = 8;  // 16-byte stripes per lane in flight
@@ -441,9 +443,9 @@ cudaError_t launch_pack_x(const void* h, int h_dtype, const float* inv, const fl
                           const PlanDev& p, int cap, void* xperm, cudaStream_t s) {
   const int grid = std::max(1, std::min(num_sms() * 8, (cap + 7) / 8));
   if (h_dtype == BEAM_BF16)
-    tc::pack_x_kernel<__nv_bfloat16><<<grid, 256, g.d_pad * sizeof(float), s>>>((const __nv_bfloat16*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
+    launch_pdl(tc::pack_x_kernel<__nv_bfloat16>, grid, 256, g.d_pad * sizeof(float), s, (const __nv_bfloat16*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
   else
-    tc::pack_x_kernel<float><<<grid, 256, g.d_pad * sizeof(float), s>>>((const float*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
+    launch_pdl(tc::pack_x_kernel<float>, grid, 256, g.d_pad * sizeof(float), s, (const float*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -464,12 +466,12 @@ cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* 
     attr = true;
   }
   Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
-  grouped_gemm_kernel<<<num_sms(), kThreads, smem, s>>>(mA1, mB1, a1);
+  launch_pdl(grouped_gemm_kernel, num_sms(), kThreads, smem, s, mA1, mB1, a1);
   count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
-  grouped_gemm_kernel<<<num_sms(), kThreads, smem, s>>>(mA2, mB2, a2);
+  launch_pdl(grouped_gemm_kernel, num_sms(), kThreads, smem, s, mA2, mB2, a2);
   count_launches(1);
   return cudaGetLastError();
 }
