@@ -247,7 +247,7 @@ int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, in
     BEAM_TRY(launch_down_simt(L, g, T, w.plan, w.act, w.opair, s));
     prof_mark(4, s);
   }
-  BEAM_TRY(launch_combine(w.plan, w.opair, T, g.Keff, g.d, g.d_pad, h, h_dtype, o->out, h_dtype, s));
+  BEAM_TRY(launch_combine(w.plan, w.opair, w.tc ? BEAM_BF16 : BEAM_F32, T, g.Keff, g.d, g.d_pad, h, h_dtype, o->out, h_dtype, s));
   prof_mark(5, s);
   return BEAM_OK;
 }
@@ -288,7 +288,7 @@ int beam_moe_execute(const beam_layer_t* layer, const void* x, int x_dtype, int 
   BEAM_TRY(strided_input(g, x, x_dtype, T, w, &X, s));
   BEAM_TRY(launch_permute<int32_t>(ids, wts, T, K, g.E, 1, w.plan, w.pscratch, s));
   BEAM_TRY(launch_experts_simt(L, g, X, x_dtype, T, w.plan, w.act, w.opair, s));
-  BEAM_TRY(launch_combine(w.plan, w.opair, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
+  BEAM_TRY(launch_combine(w.plan, w.opair, BEAM_F32, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
   return BEAM_OK;
 }
 
@@ -350,7 +350,7 @@ int beam_grouped_execute(const beam_layer_t* layer, const void* x, int x_dtype, 
   BEAM_TRY(launch_plan_prepare(counts, offsets, tokens, slots, meta, weights_hat, T, K, g.N, p,
                                flags, s));
   BEAM_TRY(launch_experts_simt(L, g, X, x_dtype, T, p, w.act, w.opair, s));
-  BEAM_TRY(launch_combine(p, w.opair, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
+  BEAM_TRY(launch_combine(p, w.opair, BEAM_F32, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
   return BEAM_OK;
 }
 

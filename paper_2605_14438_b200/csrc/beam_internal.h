@@ -130,11 +130,12 @@ bool router_tc_supported(int T, int cols, int d_pad, int x_dtype);
 size_t router_tc_scratch_bytes(int cols, int d_pad);
 cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* gate_wT, int T, int cols, int d,
                              int d_pad, float* P, void* scratch, cudaStream_t s);
+// opair written as bf16 [cap, d_pad] (combine reads it with BEAM_BF16)
 cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* xperm, const PlanDev& p,
-                              int cap, void* act16, float* opair, cudaStream_t s);
+                              int cap, void* act16, void* opair, cudaStream_t s);
 
 // combine.cu
-cudaError_t launch_combine(const PlanDev& p, const float* opair, int T, int Keff, int d, int d_pad,
+cudaError_t launch_combine(const PlanDev& p, const void* opair, int opair_dtype, int T, int Keff, int d, int d_pad,
                            const void* h, int h_dtype, void* out, int out_dtype,
                            cudaStream_t s);
 

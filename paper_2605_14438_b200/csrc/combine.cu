@@ -6,21 +6,30 @@
 // accumulates experts in ascending id (dispatch/__init__.py:145-156), then the
 // shared experts in index order (beam.py:163-164), then out = h + y (beam.py:165).
 // Shared experts are planned as ids N..N+S-1, so one ascending pass reproduces it.
-// Deterministic: a fixed sequential fp32 sum per element, no atomics.
+// Deterministic: a fixed sequential fp32 sum per element, no atomics.  The
+// per-pair rows are fp32 (decode) or bf16 (prefill: halves the HBM traffic of
+// the down-projection epilogue and this kernel; the sum stays fp32).
 #include "beam_common.cuh"
 #include "beam_internal.h"
 
 namespace beam {
 
-template <typename TH, typename TO>
+// 4 consecutive per-pair values as floats
+__device__ __forceinline__ float4 ld_pair4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ld_pair4(const __nv_bfloat16* p) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+  return make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                     __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u));
+}
+
+template <typename TH, typename TO, typename TP>
 __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict__ slot_expert,
                                                       const int32_t* __restrict__ slot_pos,
-                                                      const float* __restrict__ opair, int Keff,
-                                                      int d, int d_pad, const TH* __restrict__ h,
-                                                      TO* __restrict__ out) {
+                                                      const TP* __restrict__ opair, int Keff, int d, int d_pad,
+                                                      const TH* __restrict__ h, TO* __restrict__ out) {
   extern __shared__ int sm[];
-  int* ex = sm;              // [Keff]
-  int* ps = sm + Keff;       // [Keff]
+  int* ex = sm;                 // [Keff]
+  int* ps = sm + Keff;          // [Keff]
   int* sorted = sm + 2 * Keff;  // [Keff]
   __shared__ int nvalid_s;
   griddep_wait();
@@ -45,8 +54,8 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
   }
   __syncthreads();
   const int nv = nvalid_s;
-  // one float4 column group per thread; the (up to 8 per batch) expert rows of a
-  // group are loaded back to back, then added in ascending expert order
+  // one 4-column group per thread; the (up to 8 per batch) expert rows of a group
+  // are loaded back to back, then added in ascending expert order
   const int d4 = d_pad >> 2;
   for (int c4 = threadIdx.x; c4 < d4; c4 += blockDim.x) {
     if (4 * c4 >= d) break;
@@ -55,7 +64,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
       float4 v[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        if (r0 + q < nv) v[q] = __ldg(reinterpret_cast<const float4*>(opair + (size_t)sorted[r0 + q] * d_pad) + c4);
+        if (r0 + q < nv) v[q] = ld_pair4(opair + (size_t)sorted[r0 + q] * d_pad + 4 * c4);
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         if (r0 + q < nv) {
@@ -78,20 +87,27 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
   }
 }
 
-cudaError_t launch_combine(const PlanDev& p, const float* opair, int T, int Keff, int d, int d_pad,
-                           const void* h, int h_dtype, void* out, int out_dtype, cudaStream_t s) {
-  if (T <= 0) return cudaSuccess;
+template <typename TP>
+static cudaError_t combine_dispatch(const PlanDev& p, const TP* opair, int T, int Keff, int d, int d_pad,
+                                    const void* h, int h_dtype, void* out, int out_dtype, cudaStream_t s) {
   const size_t smem = (size_t)3 * Keff * sizeof(int);
   if (out_dtype == BEAM_F32 && h_dtype == BEAM_F32)
-    launch_pdl(combine_kernel<float, float>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const float*)h, (float*)out);
-  else if (out_dtype == BEAM_BF16 && h_dtype == BEAM_BF16)
-    launch_pdl(combine_kernel<__nv_bfloat16, __nv_bfloat16>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const __nv_bfloat16*)h, (__nv_bfloat16*)out);
-  else if (out_dtype == BEAM_F32 && h_dtype == BEAM_BF16)
-    launch_pdl(combine_kernel<__nv_bfloat16, float>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const __nv_bfloat16*)h, (float*)out);
-  else
-    launch_pdl(combine_kernel<float, __nv_bfloat16>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const float*)h, (__nv_bfloat16*)out);
+    return launch_pdl(combine_kernel<float, float, TP>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const float*)h, (float*)out);
+  if (out_dtype == BEAM_BF16 && h_dtype == BEAM_BF16)
+    return launch_pdl(combine_kernel<__nv_bfloat16, __nv_bfloat16, TP>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const __nv_bfloat16*)h, (__nv_bfloat16*)out);
+  if (out_dtype == BEAM_F32)
+    return launch_pdl(combine_kernel<__nv_bfloat16, float, TP>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const __nv_bfloat16*)h, (float*)out);
+  return launch_pdl(combine_kernel<float, __nv_bfloat16, TP>, T, 256, smem, s, p.slot_expert, p.slot_pos, opair, Keff, d, d_pad, (const float*)h, (__nv_bfloat16*)out);
+}
+
+cudaError_t launch_combine(const PlanDev& p, const void* opair, int opair_dtype, int T, int Keff, int d, int d_pad,
+                           const void* h, int h_dtype, void* out, int out_dtype, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  cudaError_t e = opair_dtype == BEAM_BF16
+                      ? combine_dispatch(p, (const __nv_bfloat16*)opair, T, Keff, d, d_pad, h, h_dtype, out, out_dtype, s)
+                      : combine_dispatch(p, (const float*)opair, T, Keff, d, d_pad, h, h_dtype, out, out_dtype, s);
   count_launches(1);
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace beam

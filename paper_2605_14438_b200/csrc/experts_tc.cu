@@ -53,7 +53,7 @@ struct Args {
   const float* w;
   __nv_bfloat16* act;
   int f_pad;
-  float* opair;
+  void* opair;  // mode 1: [cap, d_pad] bf16 per-pair rows; mode 2: fp32 logits
   int d_pad;
 };
 
@@ -142,19 +142,22 @@ struct Tile {
   int e, m_tile, a_row0, b_row0, ntok, nmma;
 };
 
-__device__ __forceinline__ Tile decode(int t, const int* tile_off, int E, int MT, const Args& a) {
-  // largest e with tile_off[e] * MT <= t
-  int lo = 0, hi = E;  // invariant: tile_off[lo]*MT <= t < tile_off[hi]*MT
+// Work unit u = (expert, m-group of CM m-tiles, n-tile); CTA `rank` of the cluster
+// takes m-tile mg*CM + rank, all CTAs of a cluster share the token (B) tile.
+__device__ __forceinline__ Tile decode(int u, const int* tile_off, int E, int MG, int CM, int rank,
+                                       const Args& a) {
+  // largest e with tile_off[e] * MG <= u
+  int lo = 0, hi = E;  // invariant: tile_off[lo]*MG <= u < tile_off[hi]*MG
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (tile_off[mid] * MT <= t) lo = mid;
+    if (tile_off[mid] * MG <= u) lo = mid;
     else hi = mid;
   }
   Tile r;
   r.e = lo;
   const int nt = tile_off[lo + 1] - tile_off[lo];
-  const int local = t - tile_off[lo] * MT;
-  r.m_tile = local / nt;
+  const int local = u - tile_off[lo] * MG;
+  r.m_tile = (local / nt) * CM + rank;
   const int n_tile = local % nt;
   r.a_row0 = lo * a.m_rows + r.m_tile * BM;
   const int tok0 = n_tile * BN;
@@ -164,6 +167,38 @@ __device__ __forceinline__ Tile decode(int t, const int* tile_off, int E, int MT
   return r;
 }
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// B box multicast to every CTA of the cluster (same smem offset, each CTA's barrier)
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+// MMA completion arrives on the barrier at the same offset in every CTA of the cluster
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+
+// CM = cluster size along M: the CTAs of a cluster compute CM consecutive m-tiles of
+// the same (expert, token tile) and share every B (token) stage through TMA
+// multicast, dividing the L2 -> SM operand traffic of B by CM.
+template <int CM>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         Args args) {
@@ -203,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CM);  // released by the MMAs of every CTA in the cluster
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -221,26 +256,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   fence_before();
-  __syncthreads();
+  if constexpr (CM > 1) cluster_sync_all();  // barrier inits visible cluster-wide
+  else __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total = tile_off[E] * MT;
+  const int rank = CM > 1 ? (int)cluster_rank() : 0;
+  const uint16_t cmask = (uint16_t)((1u << CM) - 1u);
+  const int MG = MT / CM;
+  const int total = tile_off[E] * MG;
+  const int u0 = blockIdx.x / CM, ustep = gridDim.x / CM;
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const Tile tl = decode(t, tile_off, E, MT, args);
+      for (int t = u0; t < total; t += ustep) {
+        const Tile tl = decode(t, tile_off, E, MG, CM, rank, args);
         const int nbox = (tl.nmma + kBBox - 1) / kBBox;
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], kABytes + nbox * kBBoxBytes);
           tma_load_2d(sa + stage * kABytes, &tmA, &full[stage], kb * BK, tl.a_row0);
-          for (int c = 0; c < nbox; ++c)
-            tma_load_2d(sb + stage * kBBytes + c * kBBoxBytes, &tmB, &full[stage], (kb % args.b_kblocks) * BK,
-                        tl.b_row0 + c * kBBox);
+          for (int c = 0; c < nbox; ++c) {
+            if constexpr (CM > 1) {
+              if (c % CM == rank)
+                tma_load_2d_mc(sb + stage * kBBytes + c * kBBoxBytes, &tmB, &full[stage],
+                               (kb % args.b_kblocks) * BK, tl.b_row0 + c * kBBox, cmask);
+            } else {
+              tma_load_2d(sb + stage * kBBytes + c * kBBoxBytes, &tmB, &full[stage], (kb % args.b_kblocks) * BK,
+                          tl.b_row0 + c * kBBox);
+            }
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -256,8 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const Tile tl = decode(t, tile_off, E, MT, args);
+      for (int t = u0; t < total; t += ustep) {
+        const Tile tl = decode(t, tile_off, E, MG, CM, rank, args);
         const uint32_t idesc = idesc_base | ((uint32_t)(tl.nmma >> 3) << 17);
         const uint32_t tmem_d = tmem_base + acc * BN;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -270,7 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
             mma_bf16(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-          mma_commit(&empty[stage]);
+          if constexpr (CM > 1) mma_commit_mc(&empty[stage], cmask);
+          else mma_commit(&empty[stage]);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -286,8 +334,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lane_base = 32 * (warp & 3);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const Tile tl = decode(t, tile_off, E, MT, args);
+    for (int t = u0; t < total; t += ustep) {
+      const Tile tl = decode(t, tile_off, E, MG, CM, rank, args);
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + acc * BN;
@@ -316,7 +364,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int col = c0 + j;
             if (col < tl.ntok) {
               const int pos = tl.b_row0 + col;
-              args.opair[(size_t)pos * args.d_pad + row] = v[j] * __ldg(args.w + pos);
+              reinterpret_cast<__nv_bfloat16*>(args.opair)[(size_t)pos * args.d_pad + row] =
+                  __float2bfloat16_rn(v[j] * __ldg(args.w + pos));
             }
           }
         } else {
@@ -324,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int col = c0 + j;
-            if (col < tl.ntok) args.opair[(size_t)(tl.b_row0 + col) * args.m_rows + row] = v[j];
+            if (col < tl.ntok) reinterpret_cast<float*>(args.opair)[(size_t)(tl.b_row0 + col) * args.m_rows + row] = v[j];
           }
         }
       }
@@ -336,7 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   fence_before();
-  __syncthreads();
+  if constexpr (CM > 1) cluster_sync_all();  // no CTA leaves while peers may still multicast into it
+  else __syncthreads();
   fence_after();
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
@@ -450,8 +500,52 @@ cudaError_t launch_pack_x(const void* h, int h_dtype, const float* inv, const fl
   return cudaGetLastError();
 }
 
+// Persistent launch: one CTA per SM in clusters of CM along M (CM = largest of
+// 4, 2, 1 dividing the number of 128-row m-tiles), programmatic serialization
+// with the previous kernel when `pdl`.
+template <int CM>
+static cudaError_t launch_gemm_cm(const CUtensorMap& mA, const CUtensorMap& mB, const tc::Args& a, size_t smem,
+                                  bool pdl, cudaStream_t s) {
+  using namespace tc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(grouped_gemm_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(kMaxE));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((num_sms() / CM) * CM);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  at[n].id = cudaLaunchAttributeClusterDimension;
+  at[n].val.clusterDim.x = CM;
+  at[n].val.clusterDim.y = 1;
+  at[n].val.clusterDim.z = 1;
+  ++n;
+  if (pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CM>, mA, mB, a);
+  count_launches(1);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+static cudaError_t launch_gemm(const CUtensorMap& mA, const CUtensorMap& mB, const tc::Args& a, size_t smem,
+                               bool pdl, cudaStream_t s) {
+  const int mt = a.m_rows / tc::BM;
+  if (mt % 4 == 0) return launch_gemm_cm<4>(mA, mB, a, smem, pdl, s);
+  if (mt % 2 == 0) return launch_gemm_cm<2>(mA, mB, a, smem, pdl, s);
+  return launch_gemm_cm<1>(mA, mB, a, smem, pdl, s);
+}
+
 cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* xperm, const PlanDev& p,
-                              int cap, void* act16, float* opair, cudaStream_t s) {
+                              int cap, void* act16, void* opair, cudaStream_t s) {
   using namespace tc;
   CUtensorMap mA1, mB1, mA2, mB2;
   if (!make_map(&mA1, L.w_gu, (uint64_t)g.E * 2 * g.f_pad, g.d_pad, BM) ||
@@ -460,20 +554,11 @@ cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* 
       !make_map(&mB2, act16, (uint64_t)cap, g.f_pad, kBBox))
     return cudaErrorInvalidValue;
   const size_t smem = smem_bytes(g.E);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(kMaxE));
-    attr = true;
-  }
   Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
-  launch_pdl(grouped_gemm_kernel, num_sms(), kThreads, smem, s, mA1, mB1, a1);
-  count_launches(1);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_gemm(mA1, mB1, a1, smem, true, s);
   if (e != cudaSuccess) return e;
   Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
-  launch_pdl(grouped_gemm_kernel, num_sms(), kThreads, smem, s, mA2, mB2, a2);
-  count_launches(1);
-  return cudaGetLastError();
+  return launch_gemm(mA2, mB2, a2, smem, true, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -523,15 +608,8 @@ cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* ga
   CUtensorMap mA, mB;
   if (!make_map(&mA, A3, (uint64_t)cols, 3ull * d_pad, BM) || !make_map(&mB, X, (uint64_t)T, d_pad, kBBox))
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(kMaxE));
-    attr = true;
-  }
   Args a{2, 1, cols, 3 * d_pad, d_pad / BK, plan1, plan1 + 1, nullptr, nullptr, 0, P, 0};
-  grouped_gemm_kernel<<<num_sms(), kThreads, smem_bytes(1), s>>>(mA, mB, a);
-  count_launches(1);
-  return cudaGetLastError();
+  return launch_gemm(mA, mB, a, smem_bytes(1), true, s);
 }
 
 }  // namespace beam
