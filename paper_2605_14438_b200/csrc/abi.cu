@@ -366,8 +366,9 @@ int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w,
 unsigned long long beam_kernel_launches(void) { return g_launches.load(); }
 
 int beam_set_expert_path(int mode) {
-  if (mode < 0 || mode > 2) return BEAM_ERR_ARG;
-  g_expert_path.store(mode);
+  if (mode < 0 || mode > 3) return BEAM_ERR_ARG;
+  g_expert_path.store(mode == 3 ? 2 : mode);
+  set_gemm_variant(mode == 3 ? 1 : 0);
   return BEAM_OK;
 }
 

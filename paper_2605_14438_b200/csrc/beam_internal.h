@@ -126,6 +126,7 @@ inline cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, con
 bool tc_supported(const beam_layer_t& L, const Dims& g);
 cudaError_t launch_pack_x(const void* h, int h_dtype, const float* inv, const float* nw, const Dims& g,
                           const PlanDev& p, int cap, void* xperm, cudaStream_t s);
+void set_gemm_variant(int v);  // 0 = 2-SM pairs when possible, 1 = 1-SM kernel
 bool router_tc_supported(int T, int cols, int d_pad, int x_dtype);
 size_t router_tc_scratch_bytes(int cols, int d_pad);
 cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* gate_wT, int T, int cols, int d,

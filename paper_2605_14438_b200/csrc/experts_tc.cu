@@ -392,6 +392,234 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
 }
 
+// ---------------------------------------------------------------------------
+// 2-SM variant (cta_group::2): a CTA pair computes a 256-row x N tile with one
+// tcgen05.mma issued by the leader.  Each CTA stages its own 128 weight rows and
+// HALF of the token rows, so per-SM operand traffic per FLOP drops by 1.5x vs
+// the 1-SM kernel and the ring holds 6 stages.  The TMA loads of both CTAs
+// signal the leader's full barrier; the leader's commits release both CTAs'
+// stages (multicast); both epilogues release the leader's accumulator barrier.
+// ---------------------------------------------------------------------------
+constexpr int kStages2 = 6;
+constexpr int kBHalfBytes = (BN / 2) * BK * 2;  // 16 KB: 128 token rows
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"((uint16_t)3)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                            Args args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;                                  // kStages2 x 16 KB (this CTA's 128 weight rows)
+  uint8_t* sb = smem + kStages2 * kABytes;             // kStages2 x 16 KB (this CTA's half of the tokens)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kStages2 * kBHalfBytes);
+  uint64_t* empty = full + kStages2;
+  uint64_t* tfull = empty + kStages2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* tile_off = reinterpret_cast<int*>(tmem_slot + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_rank();
+  griddep_wait();
+  const int E = args.E;
+  const int MT = args.m_rows / BM;
+  const int KB = args.K / BK;
+
+  if (warp == 0) {
+    int carry = 0;
+    if (lane == 0) tile_off[0] = 0;
+    for (int base = 0; base < E; base += 32) {
+      const int e = base + lane;
+      int v = e < E ? (args.counts[e] + BN - 1) / BN : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (e < E) tile_off[e + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(&full[s], 1);   // leader's: one expect_tx arrival + both CTAs' bytes
+      mbar_init(&empty[s], 1);  // released by the leader's multicast commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (used on the leader)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  fence_before();
+  cluster_sync_all();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int MG = MT / 2;
+  const int total = tile_off[E] * MG;
+  const int u0 = blockIdx.x / 2, ustep = gridDim.x / 2;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = u0; t < total; t += ustep) {
+        const Tile tl = decode(t, tile_off, E, MG, 2, rank, args);
+        const int half = tl.nmma >> 1;  // token rows staged by each CTA
+        const int nbox = (half + kBBox - 1) / kBBox;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t lbar = mapa_u32(smem_u32(&full[stage]), 0);
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * (kABytes + nbox * kBBoxBytes));
+          tma_load_2d_2sm(sa + stage * kABytes, &tmA, lbar, kb * BK, tl.a_row0);
+          for (int c = 0; c < nbox; ++c)
+            tma_load_2d_2sm(sb + stage * kBHalfBytes + c * kBBoxBytes, &tmB, lbar, (kb % args.b_kblocks) * BK,
+                            tl.b_row0 + rank * half + c * kBBox);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc_base = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = u0; t < total; t += ustep) {
+        const Tile tl = decode(t, tile_off, E, MG, 2, 0, args);
+        const uint32_t idesc = idesc_base | ((uint32_t)(tl.nmma >> 3) << 17);
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        fence_after();
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          const uint64_t ad = sdesc_sw128(smem_u32(sa + stage * kABytes));
+          const uint64_t bd = sdesc_sw128(smem_u32(sb + stage * kBHalfBytes));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_2sm(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          mma_commit_2sm(&empty[stage]);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_2sm(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ---------------- epilogue (both CTAs: own TMEM = own 128 rows) ----------------
+    const int lane_base = 32 * (warp & 3);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = u0; t < total; t += ustep) {
+      const Tile tl = decode(t, tile_off, E, MG, 2, rank, args);
+      mbar_wait(&tfull[acc], acc_phase);
+      fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + acc * BN;
+      for (int c0 = 0; c0 < tl.ntok; c0 += 32) {
+        float v[32];
+        tmem_ld32(tbase + c0, v);
+        if (args.mode == 0) {
+          const int b = (tl.m_tile * BM + lane_base) >> 5;
+          const int f = 16 * b + (lane & 15);
+          const bool lo = lane < 16;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float send = lo ? v[16 + j] : v[j];
+            const float r = __shfl_xor_sync(0xffffffffu, send, 16);
+            const float g = lo ? v[j] : r;
+            const float u = lo ? r : v[16 + j];
+            const int col = c0 + (lo ? j : 16 + j);
+            if (col < tl.ntok)
+              args.act[(size_t)(tl.b_row0 + col) * args.f_pad + f] = __float2bfloat16_rn(activation<BEAM_ACT_SILU>(g) * u);
+          }
+        } else if (args.mode == 1) {
+          const int row = tl.m_tile * BM + lane_base + lane;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = c0 + j;
+            if (col < tl.ntok) {
+              const int pos = tl.b_row0 + col;
+              reinterpret_cast<__nv_bfloat16*>(args.opair)[(size_t)pos * args.d_pad + row] =
+                  __float2bfloat16_rn(v[j] * __ldg(args.w + pos));
+            }
+          }
+        } else {
+          const int row = tl.m_tile * BM + lane_base + lane;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = c0 + j;
+            if (col < tl.ntok) reinterpret_cast<float*>(args.opair)[(size_t)(tl.b_row0 + col) * args.m_rows + row] = v[j];
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tempty[acc]), 0));
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  fence_before();
+  cluster_sync_all();
+  fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+}
+
 // x_n rows in plan order, bf16 (B operand of GEMM1): X[p] = bf16(h[tok_p] * inv * w)
 template <typename TX>
 __global__ void __launch_bounds__(256) pack_x_kernel(const TX* __restrict__ h, const float* __restrict__ inv,
@@ -536,13 +764,45 @@ static cudaError_t launch_gemm_cm(const CUtensorMap& mA, const CUtensorMap& mB, 
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+static size_t smem_bytes_2sm(int E) {
+  using namespace tc;
+  return 1024 + (size_t)kStages2 * (kABytes + kBHalfBytes) + (2 * kStages2 + 4) * 8 + 16 + (size_t)(E + 1) * 4;
+}
+
+static cudaError_t launch_gemm_2sm(const CUtensorMap& mA, const CUtensorMap& mB, const tc::Args& a, bool pdl,
+                                   cudaStream_t s) {
+  using namespace tc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(grouped_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes_2sm(kMaxE));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((num_sms() / 2) * 2);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes_2sm(a.E);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel, mA, mB, a);
+  count_launches(1);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// GEMM kernel choice: 0 = auto (2-SM pairs when the m-tiles pair up), 1 = 1-SM.
+static int g_gemm_variant = 0;
+
 static cudaError_t launch_gemm(const CUtensorMap& mA, const CUtensorMap& mB, const tc::Args& a, size_t smem,
                                bool pdl, cudaStream_t s) {
   const int mt = a.m_rows / tc::BM;
-  if (mt % 4 == 0) return launch_gemm_cm<4>(mA, mB, a, smem, pdl, s);
-  if (mt % 2 == 0) return launch_gemm_cm<2>(mA, mB, a, smem, pdl, s);
+  if (g_gemm_variant == 0 && mt % 2 == 0) return launch_gemm_2sm(mA, mB, a, pdl, s);
   return launch_gemm_cm<1>(mA, mB, a, smem, pdl, s);
 }
+
+void set_gemm_variant(int v) { g_gemm_variant = v; }
 
 cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* xperm, const PlanDev& p,
                               int cap, void* act16, void* opair, cudaStream_t s) {
