@@ -200,6 +200,7 @@ def beam_block_forward(h, block: MoEBlock, training: bool = True, block_size: in
 def set_expert_path(mode: str = "auto") -> None:
     """Choose the expert-stage kernels of beam_block_forward: "auto" (tcgen05
     grouped GEMM for prefill-sized batches, weight streaming for decode),
-    "simt" (weight streaming always) or "tc" (tcgen05 always, bf16 weights)."""
-    code = {"auto": 0, "simt": 1, "tc": 2}[mode]
+    "simt" (weight streaming always), "tc" (tcgen05 always, bf16 weights; 2-SM
+    CTA pairs) or "tc1" (tcgen05 always, 1-SM kernel)."""
+    code = {"auto": 0, "simt": 1, "tc": 2, "tc1": 3}[mode]
     _lib.check(_lib.load().beam_set_expert_path(code), "beam_set_expert_path")

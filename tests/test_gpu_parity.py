@@ -447,3 +447,25 @@ def test_prefill_auto_path_q30_8192():
     assert np.array_equal(_np(dec.topk_indices[sub])[ok], ref.decision.topk_indices[ok])
     o = _np(out[sub].float()).astype(np.float64)
     assert normwise_rel(o[ok], ref.out[ok]) <= TOL_BF16
+
+
+def test_tcgen05_pair_matches_single_sm():
+    """cta_group::2 (CTA pairs, M = 256) and the 1-SM kernel compute the same GEMMs."""
+    rng = np.random.default_rng(77)
+    ob = O.make_block(2048, 768, 128, 8, rng, init_std=0.02)
+    ob.mask_w = rng.normal(0, 1 / np.sqrt(2048), (2048, 128))
+    ob, gb = matched_blocks(ob, "bf16")
+    x = torch.from_numpy(rng.normal(size=(700, 2048))).to(torch.bfloat16).cuda()
+    try:
+        B.set_expert_path("tc")
+        o2, _, _ = B.beam_block_forward(x, gb, training=False)
+        B.set_expert_path("tc1")
+        o1, _, _ = B.beam_block_forward(x, gb, training=False)
+    finally:
+        B.set_expert_path("auto")
+    y2 = _np(o2.float() - x.float()).astype(np.float64)
+    y1 = _np(o1.float() - x.float()).astype(np.float64)
+    assert normwise_rel(y2, y1) <= 1e-2
+    ref = O.beam_block_forward(x.double().cpu().numpy(), ob)
+    ok = topk_margin_ok(ref.decision.logits, 8, 1e-5) & mask_margin_ok(ref, 1e-5)
+    assert normwise_rel(_np(o2.float()).astype(np.float64)[ok], ref.out[ok]) <= TOL_BF16
