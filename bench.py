@@ -354,6 +354,7 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     lib = _lib.load()
     hbm_peak, tc_peak, peak_kind = measured_peaks()
+    B.set_expert_path(args.expert_path)
     d, f, n, k = Q30["d"], Q30["f"], Q30["n"], Q30["k"]
     cfg = B.MoEBlockConfig(d_h=d, d_ff=f, num_experts=n, top_k=k)
 
@@ -492,6 +493,8 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--expert-path", default="auto", choices=("auto", "simt", "tc", "tc1"),
+                    help="expert-stage kernels (diagnostics; default auto)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

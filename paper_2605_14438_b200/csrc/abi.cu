@@ -240,6 +240,12 @@ int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, in
     BEAM_TRY(launch_experts_tc(L, g, w.xperm, w.plan, w.cap, w.act16, w.opair, s));
     prof_mark(3, s);
     prof_mark(4, s);
+  } else if (stream_supported(L, g) && g_expert_path.load() != 1) {
+    BEAM_TRY(launch_gateup_stream(L, g, X, h_dtype, L.has_norm ? w.inv : nullptr,
+                                  L.has_norm ? L.norm_w : nullptr, w.plan, w.act, s));
+    prof_mark(3, s);
+    BEAM_TRY(launch_down_stream(L, g, w.plan, w.act, w.opair, s));
+    prof_mark(4, s);
   } else {
     BEAM_TRY(launch_gateup_simt(L, g, X, h_dtype, T, L.has_norm ? w.inv : nullptr,
                                 L.has_norm ? L.norm_w : nullptr, w.plan, w.act, s));

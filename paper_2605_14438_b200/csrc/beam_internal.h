@@ -114,12 +114,32 @@ cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void*
                                cudaStream_t s);
 cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const PlanDev& p,
                              const float* act, float* opair, cudaStream_t s);
+// experts_stream.cu (bulk-copy weight streaming, bf16 weights)
+bool stream_supported(const beam_layer_t& L, const Dims& g);
+cudaError_t launch_gateup_stream(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype,
+                                 const float* inv, const float* nw, const PlanDev& p, float* act, cudaStream_t s);
+cudaError_t launch_down_stream(const beam_layer_t& L, const Dims& g, const PlanDev& p, const float* act,
+                               float* opair, cudaStream_t s);
+
+// Decode expert stage: bulk-copy streaming for bf16 weights, SIMT loads otherwise.
+inline cudaError_t launch_experts_decode(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
+                                         const float* inv, const float* nw, const PlanDev& p, float* act,
+                                         float* opair, cudaStream_t s) {
+  cudaError_t e;
+  if (stream_supported(L, g)) {
+    e = launch_gateup_stream(L, g, X, x_dtype, inv, nw, p, act, s);
+    if (e != cudaSuccess) return e;
+    return launch_down_stream(L, g, p, act, opair, s);
+  }
+  e = launch_gateup_simt(L, g, X, x_dtype, T, inv, nw, p, act, s);
+  if (e != cudaSuccess) return e;
+  return launch_down_simt(L, g, T, p, act, opair, s);
+}
+
 inline cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, const void* X,
                                        int x_dtype, int T, const PlanDev& p, float* act, float* opair,
                                        cudaStream_t s) {
-  cudaError_t e = launch_gateup_simt(L, g, X, x_dtype, T, nullptr, nullptr, p, act, s);
-  if (e != cudaSuccess) return e;
-  return launch_down_simt(L, g, T, p, act, opair, s);
+  return launch_experts_decode(L, g, X, x_dtype, T, nullptr, nullptr, p, act, opair, s);
 }
 
 // experts_tc.cu (tcgen05 grouped GEMM, prefill)
