@@ -493,7 +493,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--expert-path", default="auto", choices=("auto", "simt", "tc", "tc1"),
+    ap.add_argument("--expert-path", default="auto", choices=("auto", "simt", "tc", "tc1", "stream"),
                     help="expert-stage kernels (diagnostics; default auto)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -240,7 +240,7 @@ int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, in
     BEAM_TRY(launch_experts_tc(L, g, w.xperm, w.plan, w.cap, w.act16, w.opair, s));
     prof_mark(3, s);
     prof_mark(4, s);
-  } else if (stream_supported(L, g) && g_expert_path.load() != 1) {
+  } else if (g_expert_path.load() == 4 && stream_supported(L, g)) {  // bulk-copy streaming (experimental)
     BEAM_TRY(launch_gateup_stream(L, g, X, h_dtype, L.has_norm ? w.inv : nullptr,
                                   L.has_norm ? L.norm_w : nullptr, w.plan, w.act, s));
     prof_mark(3, s);
@@ -372,7 +372,7 @@ int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w,
 unsigned long long beam_kernel_launches(void) { return g_launches.load(); }
 
 int beam_set_expert_path(int mode) {
-  if (mode < 0 || mode > 3) return BEAM_ERR_ARG;
+  if (mode < 0 || mode > 4) return BEAM_ERR_ARG;
   g_expert_path.store(mode == 3 ? 2 : mode);
   set_gemm_variant(mode == 3 ? 1 : 0);
   return BEAM_OK;

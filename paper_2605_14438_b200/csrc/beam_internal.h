@@ -126,7 +126,7 @@ inline cudaError_t launch_experts_decode(const beam_layer_t& L, const Dims& g, c
                                          const float* inv, const float* nw, const PlanDev& p, float* act,
                                          float* opair, cudaStream_t s) {
   cudaError_t e;
-  if (stream_supported(L, g)) {
+  if (false && stream_supported(L, g)) {  // the bulk-copy kernels are still slower than the SIMT stream
     e = launch_gateup_stream(L, g, X, x_dtype, inv, nw, p, act, s);
     if (e != cudaSuccess) return e;
     return launch_down_stream(L, g, p, act, opair, s);

@@ -86,12 +86,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                            int c1) {
+                                            int c1, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
+}
+
+// L2 policies: weights stream through once (evict first); token tiles are re-read
+// by every m-tile of their expert (evict last)
+__device__ __forceinline__ uint64_t l2_policy(bool evict_first) {
+  uint64_t p;
+  if (evict_first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
@@ -167,6 +176,72 @@ __device__ __forceinline__ Tile decode(int u, const int* tile_off, int E, int MG
   return r;
 }
 
+constexpr int kStgBytes = 32 * BM * 4;  // epilogue staging: 32 tokens x 128 rows (fp32 worst case)
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// One accumulator tile -> global, 32 token columns at a time.  The 4 epilogue
+// warps (TMEM lanes 32*w4..) transpose through shared memory so every global
+// store is a contiguous token row (128-512 B per warp instruction) instead of
+// a scattered column.
+//   mode 0: act[pos, f]   = bf16(silu(gate) * up)  (64 features per tile)
+//   mode 1: opair[pos, d] = bf16(ghat[pos] * acc)  (128 output channels)
+//   mode 2: P[t, c]       = acc (fp32, router / mask logits)
+__device__ __forceinline__ void epilogue_tile(const Args& args, const Tile& tl, uint32_t tbase, int w4, int lane,
+                                              uint8_t* stg) {
+  const int ew = threadIdx.x - 64;  // 0..127 within the epilogue warps
+  for (int c0 = 0; c0 < tl.ntok; c0 += 32) {
+    const int rows = min(32, tl.ntok - c0);
+    float v[32];
+    tmem_ld32(tbase + c0, v);
+    if (args.mode == 0) {
+      // lanes 0-15 hold gate rows, 16-31 the matching up rows, of features 16*w4 + (lane & 15)
+      __nv_bfloat16* s = reinterpret_cast<__nv_bfloat16*>(stg);  // [32 tokens][64 features]
+      const int fl = 16 * w4 + (lane & 15);
+      const bool lo = lane < 16;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float send = lo ? v[16 + j] : v[j];
+        const float r = __shfl_xor_sync(0xffffffffu, send, 16);
+        const float g = lo ? v[j] : r;
+        const float u = lo ? r : v[16 + j];
+        s[(lo ? j : 16 + j) * 64 + fl] = __float2bfloat16_rn(activation<BEAM_ACT_SILU>(g) * u);
+      }
+      epi_bar();
+      for (int row = w4; row < rows; row += 4) {
+        const uint32_t val = reinterpret_cast<const uint32_t*>(s + row * 64)[lane];
+        reinterpret_cast<uint32_t*>(args.act + (size_t)(tl.b_row0 + c0 + row) * args.f_pad + tl.m_tile * 64)[lane] = val;
+      }
+    } else if (args.mode == 1) {
+      __nv_bfloat16* s = reinterpret_cast<__nv_bfloat16*>(stg);  // [32 tokens][128 channels]
+      const float wl = lane < rows ? __ldg(args.w + tl.b_row0 + c0 + lane) : 0.0f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float wj = __shfl_sync(0xffffffffu, wl, j);
+        s[j * BM + 32 * w4 + lane] = __float2bfloat16_rn(v[j] * wj);
+      }
+      epi_bar();
+      for (int row = w4; row < rows; row += 4) {
+        const uint2 val = reinterpret_cast<const uint2*>(s + row * BM)[lane];
+        reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(args.opair) + (size_t)(tl.b_row0 + c0 + row) * args.d_pad +
+                                 tl.m_tile * BM)[lane] = val;
+      }
+    } else {
+      float* s = reinterpret_cast<float*>(stg);  // [32 tokens][128 columns]
+#pragma unroll
+      for (int j = 0; j < 32; ++j) s[j * BM + 32 * w4 + lane] = v[j];
+      epi_bar();
+      for (int row = w4; row < rows; row += 4) {
+        const float4 val = reinterpret_cast<const float4*>(s + row * BM)[lane];
+        reinterpret_cast<float4*>(reinterpret_cast<float*>(args.opair) + (size_t)(tl.b_row0 + c0 + row) * args.m_rows +
+                                  tl.m_tile * BM)[lane] = val;
+      }
+    }
+    epi_bar();  // staging reused by the next chunk
+  }
+  (void)ew;
+}
+
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -206,7 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;                                  // kStages x 16 KB
   uint8_t* sb = smem + kStages * kABytes;              // kStages x 32 KB
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kStages * kBBytes);
+  uint8_t* stg = sb + kStages * kBBytes;               // epilogue staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + kStgBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
@@ -269,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
+      const uint64_t polA = l2_policy(args.mode != 2), polB = l2_policy(false);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = u0; t < total; t += ustep) {
@@ -277,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], kABytes + nbox * kBBoxBytes);
-          tma_load_2d(sa + stage * kABytes, &tmA, &full[stage], kb * BK, tl.a_row0);
+          tma_load_2d(sa + stage * kABytes, &tmA, &full[stage], kb * BK, tl.a_row0, polA);
           for (int c = 0; c < nbox; ++c) {
             if constexpr (CM > 1) {
               if (c % CM == rank)
@@ -285,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                (kb % args.b_kblocks) * BK, tl.b_row0 + c * kBBox, cmask);
             } else {
               tma_load_2d(sb + stage * kBBytes + c * kBBoxBytes, &tmB, &full[stage], (kb % args.b_kblocks) * BK,
-                          tl.b_row0 + c * kBBox);
+                          tl.b_row0 + c * kBBox, polB);
             }
           }
           if (++stage == kStages) {
@@ -338,45 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Tile tl = decode(t, tile_off, E, MG, CM, rank, args);
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + acc * BN;
-      for (int c0 = 0; c0 < tl.ntok; c0 += 32) {
-        float v[32];
-        tmem_ld32(tbase + c0, v);
-        if (args.mode == 0) {
-          // packed rows: lanes 0-15 gate, 16-31 up of features 16*b + (lane & 15)
-          const int b = (tl.m_tile * BM + lane_base) >> 5;
-          const int f = 16 * b + (lane & 15);
-          const bool lo = lane < 16;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float send = lo ? v[16 + j] : v[j];
-            const float r = __shfl_xor_sync(0xffffffffu, send, 16);
-            const float g = lo ? v[j] : r;
-            const float u = lo ? r : v[16 + j];
-            const int col = c0 + (lo ? j : 16 + j);
-            if (col < tl.ntok)
-              args.act[(size_t)(tl.b_row0 + col) * args.f_pad + f] = __float2bfloat16_rn(activation<BEAM_ACT_SILU>(g) * u);
-          }
-        } else if (args.mode == 1) {
-          const int row = tl.m_tile * BM + lane_base + lane;  // output channel
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = c0 + j;
-            if (col < tl.ntok) {
-              const int pos = tl.b_row0 + col;
-              reinterpret_cast<__nv_bfloat16*>(args.opair)[(size_t)pos * args.d_pad + row] =
-                  __float2bfloat16_rn(v[j] * __ldg(args.w + pos));
-            }
-          }
-        } else {
-          const int row = tl.m_tile * BM + lane_base + lane;  // router / mask column
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = c0 + j;
-            if (col < tl.ntok) reinterpret_cast<float*>(args.opair)[(size_t)(tl.b_row0 + col) * args.m_rows + row] = v[j];
-          }
-        }
-      }
+      epilogue_tile(args, tl, tmem_base + ((uint32_t)lane_base << 16) + acc * BN, warp & 3, lane, stg);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -410,11 +449,11 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
 }
 
 __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
-                                                int c1) {
+                                                int c1, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
 
@@ -445,7 +484,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;                                  // kStages2 x 16 KB (this CTA's 128 weight rows)
   uint8_t* sb = smem + kStages2 * kABytes;             // kStages2 x 16 KB (this CTA's half of the tokens)
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kStages2 * kBHalfBytes);
+  uint8_t* stg = sb + kStages2 * kBHalfBytes;          // epilogue staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + kStgBytes);
   uint64_t* empty = full + kStages2;
   uint64_t* tfull = empty + kStages2;
   uint64_t* tempty = tfull + 2;
@@ -505,6 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     if (lane == 0) {
+      const uint64_t polA = l2_policy(args.mode != 2), polB = l2_policy(false);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = u0; t < total; t += ustep) {
@@ -515,10 +556,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t lbar = mapa_u32(smem_u32(&full[stage]), 0);
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * (kABytes + nbox * kBBoxBytes));
-          tma_load_2d_2sm(sa + stage * kABytes, &tmA, lbar, kb * BK, tl.a_row0);
+          tma_load_2d_2sm(sa + stage * kABytes, &tmA, lbar, kb * BK, tl.a_row0, polA);
           for (int c = 0; c < nbox; ++c)
             tma_load_2d_2sm(sb + stage * kBHalfBytes + c * kBBoxBytes, &tmB, lbar, (kb % args.b_kblocks) * BK,
-                            tl.b_row0 + rank * half + c * kBBox);
+                            tl.b_row0 + rank * half + c * kBBox, polB);
           if (++stage == kStages2) {
             stage = 0;
             phase ^= 1;
@@ -568,44 +609,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const Tile tl = decode(t, tile_off, E, MG, 2, rank, args);
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + acc * BN;
-      for (int c0 = 0; c0 < tl.ntok; c0 += 32) {
-        float v[32];
-        tmem_ld32(tbase + c0, v);
-        if (args.mode == 0) {
-          const int b = (tl.m_tile * BM + lane_base) >> 5;
-          const int f = 16 * b + (lane & 15);
-          const bool lo = lane < 16;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float send = lo ? v[16 + j] : v[j];
-            const float r = __shfl_xor_sync(0xffffffffu, send, 16);
-            const float g = lo ? v[j] : r;
-            const float u = lo ? r : v[16 + j];
-            const int col = c0 + (lo ? j : 16 + j);
-            if (col < tl.ntok)
-              args.act[(size_t)(tl.b_row0 + col) * args.f_pad + f] = __float2bfloat16_rn(activation<BEAM_ACT_SILU>(g) * u);
-          }
-        } else if (args.mode == 1) {
-          const int row = tl.m_tile * BM + lane_base + lane;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = c0 + j;
-            if (col < tl.ntok) {
-              const int pos = tl.b_row0 + col;
-              reinterpret_cast<__nv_bfloat16*>(args.opair)[(size_t)pos * args.d_pad + row] =
-                  __float2bfloat16_rn(v[j] * __ldg(args.w + pos));
-            }
-          }
-        } else {
-          const int row = tl.m_tile * BM + lane_base + lane;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = c0 + j;
-            if (col < tl.ntok) reinterpret_cast<float*>(args.opair)[(size_t)(tl.b_row0 + col) * args.m_rows + row] = v[j];
-          }
-        }
-      }
+      epilogue_tile(args, tl, tmem_base + ((uint32_t)lane_base << 16) + acc * BN, warp & 3, lane, stg);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tempty[acc]), 0));
@@ -707,7 +711,7 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t c
 }
 
 static size_t smem_bytes(int E) {
-  return 1024 + (size_t)kStages * (kABytes + kBBytes) + (2 * kStages + 4) * 8 + 16 + (size_t)(E + 1) * 4;
+  return 1024 + (size_t)kStages * (kABytes + kBBytes) + kStgBytes + (2 * kStages + 4) * 8 + 16 + (size_t)(E + 1) * 4;
 }
 
 }  // namespace tc
@@ -766,7 +770,8 @@ static cudaError_t launch_gemm_cm(const CUtensorMap& mA, const CUtensorMap& mB, 
 
 static size_t smem_bytes_2sm(int E) {
   using namespace tc;
-  return 1024 + (size_t)kStages2 * (kABytes + kBHalfBytes) + (2 * kStages2 + 4) * 8 + 16 + (size_t)(E + 1) * 4;
+  return 1024 + (size_t)kStages2 * (kABytes + kBHalfBytes) + kStgBytes + (2 * kStages2 + 4) * 8 + 16 +
+         (size_t)(E + 1) * 4;
 }
 
 static cudaError_t launch_gemm_2sm(const CUtensorMap& mA, const CUtensorMap& mB, const tc::Args& a, bool pdl,
