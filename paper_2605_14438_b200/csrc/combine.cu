@@ -54,32 +54,50 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
   }
   __syncthreads();
   const int nv = nvalid_s;
-  // one 4-column group per thread; the (up to 8 per batch) expert rows of a group
-  // are loaded back to back, then added in ascending expert order
-  const int d4 = d_pad >> 2;
-  for (int c4 = threadIdx.x; c4 < d4; c4 += blockDim.x) {
-    if (4 * c4 >= d) break;
-    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int r0 = 0; r0 < nv; r0 += 8) {
-      float4 v[8];
+  // one 8-column group per thread (16-byte loads of bf16 rows); the (up to 8 per
+  // batch) expert rows of a group are loaded back to back, then added in
+  // ascending expert order
+  const int d8 = d_pad >> 3;
+  for (int c8 = threadIdx.x; c8 < d8; c8 += blockDim.x) {
+    if (8 * c8 >= d) break;
+    float y[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (r0 + q < nv) v[q] = ld_pair4(opair + (size_t)sorted[r0 + q] * d_pad + 4 * c4);
+    for (int q = 0; q < 8; ++q) y[q] = 0.0f;
+    for (int r0 = 0; r0 < nv; r0 += 8) {
+      float4 v[8][2];
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         if (r0 + q < nv) {
-          y.x += v[q].x;
-          y.y += v[q].y;
-          y.z += v[q].z;
-          y.w += v[q].w;
+          const TP* row = opair + (size_t)sorted[r0 + q] * d_pad + 8 * c8;
+          if constexpr (sizeof(TP) == 2) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(row));
+            v[q][0] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                                  __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+            v[q][1] = make_float4(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xffff0000u),
+                                  __uint_as_float(u.w << 16), __uint_as_float(u.w & 0xffff0000u));
+          } else {
+            v[q][0] = ld_pair4(row);
+            v[q][1] = ld_pair4(row + 4);
+          }
+        }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (r0 + q < nv) {
+          y[0] += v[q][0].x;
+          y[1] += v[q][0].y;
+          y[2] += v[q][0].z;
+          y[3] += v[q][0].w;
+          y[4] += v[q][1].x;
+          y[5] += v[q][1].y;
+          y[6] += v[q][1].z;
+          y[7] += v[q][1].w;
         }
     }
-    const float yy[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c = 4 * c4 + q;
+    for (int q = 0; q < 8; ++q) {
+      const int c = 8 * c8 + q;
       if (c < d) {
-        float o = yy[q];
+        float o = y[q];
         if (h != nullptr) o = to_f32<TH>(h[(size_t)t * d + c]) + o;
         out[(size_t)t * d + c] = from_f32<TO>(o);
       }

@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  permute_block<int32_t, 8, true>(a.ids32, a.gw, T, a.K + a.S, E, bs, p, reinterpret_cast<int*>(xs));
+  permute_block<int32_t, 8, true, false>(a.ids32, a.gw, T, a.K + a.S, E, bs, p, reinterpret_cast<int*>(xs));
   if (threadIdx.x == 0) counters[kCounterSlots - 1] = 0;
 }
 
@@ -395,7 +395,7 @@ cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, c
   const int kr = gemv_kr(T, cols, d_pad, kFusedMaxSplit, kFusedTT);
   dim3 grid(ceil_div(cols, 8 * kGemvCols), ceil_div(d_pad, kr), ceil_div(T, kFusedTT));
   if ((int)grid.y > kFusedMaxSplit || (int)grid.z > kCounterSlots - 1) return cudaErrorInvalidValue;
-  const size_t smem = std::max((size_t)kFusedTT * kr * sizeof(float), (size_t)(8 * E + E + 1 + 32) * sizeof(int));
+  const size_t smem = std::max((size_t)kFusedTT * kr * sizeof(float), (size_t)(8 * E + 2 * E + 1 + 32) * sizeof(int));
   const int npl = ceil_div(a.N, 32);
   cudaError_t e;
 #define BEAM_FUSED(TX_)                                                                                        \

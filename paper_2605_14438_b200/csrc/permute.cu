@@ -194,7 +194,7 @@ cudaError_t launch_permute(const IdT* ids, const float* w, int T, int K, int E, 
   if (E > kPermuteThreads || bs < 1) return cudaErrorInvalidValue;
   const long long M = (long long)T * K;
   if (M <= kSingleCtaMax || scratch == nullptr) {
-    const size_t smem = (size_t)(kPermuteWarps * E + E + 1 + 32) * sizeof(int);
+    const size_t smem = (size_t)(kPermuteWarps * E + 2 * E + 1 + 32) * sizeof(int);
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(permute_kernel<IdT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

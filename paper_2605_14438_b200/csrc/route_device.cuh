@@ -197,13 +197,15 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* scratch, int* to
 // bases (expert-major / warp-minor scan) -> ordered re-walk ranking equal experts
 // inside each 32-entry step with __match_any_sync.  Identical to the reference's
 // order (ascending flat index inside an expert) whatever the scheduling.
-// smem: NW*E + E + 1 + 32 ints.
-template <typename IdT, int NW, bool CG>
+// smem: NW*E + 2E + 1 + 32 ints.  PAD = write the -1 padding of every expert run
+// (the layer's own kernels never read it; the align_block API does).
+template <typename IdT, int NW, bool CG, bool PAD = true>
 __device__ __forceinline__ void permute_block(const IdT* __restrict__ ids, const float* __restrict__ w,
                                               int T, int K, int E, int bs, const PlanDev& p, int* smem) {
   int* hist = smem;                 // [NW][E]
   int* off_s = hist + NW * E;       // [E + 1]
   int* scratch = off_s + E + 1;     // [32]
+  int* cnt_s = scratch + 32;        // [E]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = T * K;
 
@@ -228,6 +230,7 @@ __device__ __forceinline__ void permute_block(const IdT* __restrict__ ids, const
       run += c;
     }
     p.counts[e] = run;
+    cnt_s[e] = run;
     off_s[e] = run;  // temporarily: count
   }
   __syncthreads();
@@ -281,12 +284,14 @@ __device__ __forceinline__ void permute_block(const IdT* __restrict__ ids, const
     __syncwarp();
   }
 
-  for (int e = warp; e < E; e += NW) {
-    const int real_end = off_s[e] + p.counts[e];
-    for (int q = real_end + lane; q < off_s[e + 1]; q += 32) {
-      p.tok[q] = -1;
-      p.slot[q] = -1;
-      if (p.w) p.w[q] = 0.0f;
+  if constexpr (PAD) {
+    for (int e = warp; e < E; e += NW) {
+      const int real_end = off_s[e] + cnt_s[e];
+      for (int q = real_end + lane; q < off_s[e + 1]; q += 32) {
+        p.tok[q] = -1;
+        p.slot[q] = -1;
+        if (p.w) p.w[q] = 0.0f;
+      }
     }
   }
 }
