@@ -146,6 +146,7 @@ static int validate(const beam_layer_t* L) {
   if (L->wdtype != BEAM_BF16 && L->wdtype != BEAM_F32) return BEAM_ERR_ARG;
   if (L->activation != BEAM_ACT_SILU && L->activation != BEAM_ACT_IDENTITY) return BEAM_ERR_ARG;
   if (L->num_experts > 512 || L->num_experts + L->num_shared > 1024) return BEAM_ERR_UNSUPPORTED;
+  if (L->top_k + L->num_shared > 32) return BEAM_ERR_UNSUPPORTED;  // combine: one lane per slot
   if (!L->gate_wT || !L->w_gu || !L->w_down) return BEAM_ERR_ARG;
   if (L->has_norm && !L->norm_w) return BEAM_ERR_ARG;
   return BEAM_OK;
@@ -283,6 +284,7 @@ int beam_moe_execute(const beam_layer_t* layer, const void* x, int x_dtype, int 
   int rc = validate(layer);
   if (rc) return rc;
   if (T < 0 || K < 1 || (T > 0 && (!x || !ids || !wts || !y))) return BEAM_ERR_ARG;
+  if (K > 32) return BEAM_ERR_UNSUPPORTED;
   if (x_dtype != BEAM_F32 && x_dtype != BEAM_BF16) return BEAM_ERR_ARG;
   if (T == 0) return BEAM_OK;
   const beam_layer_t& L = *layer;
@@ -334,6 +336,7 @@ int beam_grouped_execute(const beam_layer_t* layer, const void* x, int x_dtype, 
   int rc = validate(layer);
   if (rc) return rc;
   if (T < 0 || K < 1 || block_size < 1) return BEAM_ERR_ARG;
+  if (K > 32) return BEAM_ERR_UNSUPPORTED;
   if (x_dtype != BEAM_F32 && x_dtype != BEAM_BF16) return BEAM_ERR_ARG;
   if (T == 0) return BEAM_OK;
   if (!x || !counts || !offsets || !tokens || !slots || !active || !meta || !weights_hat || !y)

@@ -327,19 +327,6 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_warp_kernel(const TW* __re
     const TW* W = Wgu + (size_t)e * 2 * f_pad * d_pad;
     const int feat0 = g * 4;
     const int row_g = (feat0 >> 4) * 32 + (feat0 & 15);
-    {  // pull this warp's NEXT item into L2 while the current one streams (DRAM -> L2 latency overlap)
-      const long long nx = item + nwarps;
-      if (nx < total) {
-        const int na = (int)(nx / groups), ng = (int)(nx % groups);
-        const int nf = ng * 4;
-        const char* nb = reinterpret_cast<const char*>(Wgu + ((size_t)p.active[na] * 2 * f_pad + (nf >> 4) * 32 + (nf & 15)) * d_pad);
-        const int row_bytes = d_pad * (int)sizeof(TW);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          for (int o = lane * 128; o < row_bytes; o += 32 * 128)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + (size_t)((q & 3) + (q >> 2) * 16) * row_bytes + o));
-      }
-    }
     for (int t0 = 0; t0 < cnt;) {
       const int r = cnt - t0;
       if (r >= 3) {
@@ -422,15 +409,6 @@ __global__ void __launch_bounds__(kThreads, 2) down_warp_kernel(const TW* __rest
     const int e = p.active[a];
     const int cnt = p.counts[e], off = p.offsets[e];
     const TW* W = Wd + (size_t)e * d_pad * f_pad;
-    {  // L2 prefetch of this warp's next item (8 contiguous rows)
-      const long long nx = item + nwarps;
-      if (nx < total) {
-        const int na = (int)(nx / groups), ng = (int)(nx % groups);
-        const char* nb = reinterpret_cast<const char*>(Wd + ((size_t)p.active[na] * d_pad + ng * 8) * f_pad);
-        const int bytes = 8 * f_pad * (int)sizeof(TW);
-        for (int o = lane * 128; o < bytes; o += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + o));
-      }
-    }
     for (int t0 = 0; t0 < cnt;) {
       const int r = cnt - t0;
       if (r >= 3) {
