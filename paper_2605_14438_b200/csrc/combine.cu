@@ -8,10 +8,12 @@
 // Shared experts are planned as ids N..N+S-1, so one ascending pass reproduces it.
 // Deterministic: a fixed sequential fp32 sum per element, no atomics.
 //
-// One warp per token (8 tokens per CTA): the warp ranks the token's <= 32 slots
-// by expert id with shuffles (no shared memory, no CTA barrier), then sweeps the
-// row 8 columns per lane with 16-byte loads of the per-pair rows (fp32 on the
-// decode path, bf16 on the prefill path: the sum stays fp32).
+// One warp per (token, 256-column chunk), 8 tokens per CTA, grid.y = column
+// chunks (so a 64-token decode step still spreads over 64 CTAs): the warp ranks
+// the token's <= 32 slots by expert id with shuffles (no shared memory, no CTA
+// barrier), then each lane sums 8 columns with 16-byte loads of the per-pair
+// rows (fp32 on the decode path, bf16 on the prefill path: the sum stays fp32),
+// all rows' loads in flight before the ordered adds.
 #include "beam_common.cuh"
 #include "beam_internal.h"
 
@@ -61,19 +63,20 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const int32
     const int ej = __shfl_sync(0xffffffffu, e, j);
     if (ej >= 0 && rj == lane) sorted_pos = pj;
   }
-  for (int c0 = 8 * lane; c0 < d; c0 += 256) {
+  {
+    const int c0 = blockIdx.y * 256 + 8 * lane;
     float y[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) y[q] = 0.0f;
-    for (int r0 = 0; r0 < nv; r0 += 4) {
-      float v[4][8];
+    for (int r0 = 0; r0 < nv; r0 += 8) {
+      float v[8][8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         const int pr = __shfl_sync(0xffffffffu, sorted_pos, r0 + q < nv ? r0 + q : 0);
-        if (r0 + q < nv) ld_pair8<TP>(opair + (size_t)pr * d_pad + c0, v[q]);
+        if (r0 + q < nv && c0 < d) ld_pair8<TP>(opair + (size_t)pr * d_pad + c0, v[q]);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 8; ++q)
         if (r0 + q < nv) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) y[i] += v[q][i];
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const int32
 template <typename TP>
 static cudaError_t combine_dispatch(const PlanDev& p, const TP* opair, int T, int Keff, int d, int d_pad,
                                     const void* h, int h_dtype, void* out, int out_dtype, cudaStream_t s) {
-  const int grid = ceil_div(T, kCombineWarps);
+  const dim3 grid(ceil_div(T, kCombineWarps), ceil_div(d, 256));
   const int thr = 32 * kCombineWarps;
   if (out_dtype == BEAM_F32 && h_dtype == BEAM_F32)
     return launch_pdl(combine_kernel<float, float, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const float*)h, (float*)out);

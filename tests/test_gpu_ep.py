@@ -47,9 +47,13 @@ def test_ep_single_rank_matches_layer(nccl_group, t):
     ep = EPBeamLayer(gb)
     out_ep = ep.forward(x)
     out, _, _ = B.beam_block_forward(x, gb, training=False)
-    y_ep = (out_ep.float() - x.float()).cpu().double().numpy()
-    y = (out.float() - x.float()).cpu().double().numpy()
-    assert normwise_rel(y_ep, y) <= 2e-2
+    # out = h + y is rounded to bf16, so y recovered as out - h carries up to one
+    # bf16 ulp of |out| per element on top of the expert-sum differences
+    o_ep = out_ep.float().cpu().double().numpy()
+    o = out.float().cpu().double().numpy()
+    assert np.all(np.abs(o_ep - o) <= 2.0 ** -7 * np.abs(o) + 1e-3)
+    y_ep, y = o_ep - x.float().cpu().double().numpy(), o - x.float().cpu().double().numpy()
+    assert normwise_rel(y_ep, y) <= 6e-2
     ref = O.beam_block_forward(x.double().cpu().numpy(), ob)
     ok = topk_margin_ok(ref.decision.logits, 8, 1e-5) & mask_margin_ok(ref, 1e-5)
     assert normwise_rel(out_ep.float().cpu().double().numpy()[ok], ref.out[ok]) <= 1e-2
