@@ -37,6 +37,7 @@ EXPORTS = (
     "beam_set_expert_path",
     "beam_profile_begin",
     "beam_profile_end",
+    "beam_trace_gate",
     "beam_last_cuda_error",
     "beam_build_info",
 )
@@ -108,6 +109,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_set_expert_path": (I, [I]),
         "beam_profile_begin": (I, [I]),
         "beam_profile_end": (I, [P, P]),
+        "beam_trace_gate": (I, [P]),
         "beam_last_cuda_error": (ctypes.c_char_p, []),
         "beam_build_info": (ctypes.c_char_p, []),
     }

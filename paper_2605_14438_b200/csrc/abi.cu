@@ -413,6 +413,8 @@ int beam_profile_end(float* stage_ms, int* calls) {
   return BEAM_OK;
 }
 
+int beam_trace_gate(unsigned long long* dev_buf) { return status(beam::set_gate_trace(dev_buf)); }
+
 const char* beam_last_cuda_error(void) { return g_last_error; }
 
 #define BEAM_STR2(x) #x

@@ -160,4 +160,6 @@ cudaError_t launch_combine(const PlanDev& p, const void* opair, int opair_dtype,
                            const void* h, int h_dtype, void* out, int out_dtype,
                            cudaStream_t s);
 
+cudaError_t set_gate_trace(unsigned long long* buf);
+
 }  // namespace beam

@@ -435,56 +435,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 2-SM variant (cta_group::2): a CTA pair computes a 256-row x N tile with one
 // tcgen05.mma issued by the leader.  Each CTA stages its own 128 weight rows and
 // HALF of the token rows, so per-SM operand traffic per FLOP drops by 1.5x vs
-// the 1-SM kernel.  The TMA loads of both CTAs signal the leader's full barrier;
-// the leader's commits release both CTAs' stages (multicast); both epilogues
-// release the leader's accumulator barrier.
-//
-// Token tiles hold up to 512 tokens (an expert's tokens split into
-// ceil(count/512) balanced tiles): a tile of more than 256 tokens spans BOTH
-// 256-column TMEM accumulators, so every weight k-block is staged once per
-// (expert, m-pair) and feeds two MMAs.  Units of <= 256 tokens take one
-// accumulator and overlap their epilogue with the next unit's main loop.  The
-// accumulators are a 2-slot ring taken in order by the MMA warp and drained in
-// the same order by the epilogue.
+// the 1-SM kernel and the ring holds 6 stages.  The TMA loads of both CTAs
+// signal the leader's full barrier; the leader's commits release both CTAs'
+// stages (multicast); both epilogues release the leader's accumulator barrier.
 // ---------------------------------------------------------------------------
-constexpr int kStages2 = 4;
-constexpr int kBN2 = 512;  // tokens per 2-SM unit (two accumulators)
-constexpr int kBHalfBytes = (BN / 2) * BK * 2;  // 16 KB: 128 token rows (one accumulator)
-constexpr int kBStage2 = 2 * kBHalfBytes;        // 32 KB: this CTA's rows of both accumulators
-
-// Balanced token-tile width for an expert with cnt tokens: ceil(cnt/512) tiles'
-// worth, rounded up to the MMA's N granule; the tile count is ceil(cnt / width),
-// so no tile is empty.
-__device__ __forceinline__ int tile_width2(int cnt) {
-  const int nt = (cnt + kBN2 - 1) / kBN2;
-  return nt > 0 ? (((cnt + nt - 1) / nt + 15) & ~15) : kBN2;
-}
-
-// 2-SM work unit u = (expert, m-pair, token tile of <= 512); tile_off counts
-// token tiles per expert.
-__device__ __forceinline__ Tile decode2(int u, const int* tile_off, int E, int MG, int rank, const Args& a) {
-  int lo = 0, hi = E;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (tile_off[mid] * MG <= u) lo = mid;
-    else hi = mid;
-  }
-  Tile r;
-  r.e = lo;
-  const int nt = tile_off[lo + 1] - tile_off[lo];
-  const int local = u - tile_off[lo] * MG;
-  r.m_tile = (local / nt) * 2 + rank;
-  const int n_tile = local % nt;
-  const int cnt = a.counts[lo];
-  const int per = tile_width2(cnt);
-  r.a_row0 = lo * a.m_rows + r.m_tile * BM;
-  const int tok0 = n_tile * per;
-  r.ntok = min(per, cnt - tok0);
-  r.b_row0 = a.offsets[lo] + tok0;
-  r.nmma = (r.ntok + 15) & ~15;
-  return r;
-}
-
+constexpr int kStages2 = 6;
+constexpr int kBHalfBytes = (BN / 2) * BK * 2;  // 16 KB: 128 token rows
 
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
   uint32_t r;
@@ -500,6 +456,17 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+
+// Weight tile -> L2 only (no smem, no barrier): issued kPrefetch k-blocks ahead of
+// the staged loads so the HBM latency of the weight stream is not bounded by the
+// smem ring depth.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+constexpr int kPrefetch = 16;
 
 __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                              uint32_t accumulate) {
@@ -527,8 +494,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;                                  // kStages2 x 16 KB (this CTA's 128 weight rows)
-  uint8_t* sb = smem + kStages2 * kABytes;             // kStages2 x 32 KB (this CTA's half of the tokens)
-  uint8_t* stg = sb + kStages2 * kBStage2;             // epilogue staging
+  uint8_t* sb = smem + kStages2 * kABytes;             // kStages2 x 16 KB (this CTA's half of the tokens)
+  uint8_t* stg = sb + kStages2 * kBHalfBytes;          // epilogue staging
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + kStgBytes);
   uint64_t* empty = full + kStages2;
   uint64_t* tfull = empty + kStages2;
@@ -548,11 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (lane == 0) tile_off[0] = 0;
     for (int base = 0; base < E; base += 32) {
       const int e = base + lane;
-      int v = 0;
-      if (e < E) {
-        const int cnt = args.counts[e];
-        v = (cnt + tile_width2(cnt) - 1) / tile_width2(cnt);
-      }
+      int v = e < E ? (args.counts[e] + BN - 1) / BN : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, v, o);
@@ -596,23 +559,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t polA = l2_policy(args.mode != 2), polB = l2_policy(false);
       int stage = 0;
       uint32_t phase = 0;
+      // L2 prefetch cursor for this CTA's weight rows, kPrefetch k-blocks ahead
+      int pf_t = u0, pf_kb = 0, pf_row = u0 < total ? decode(u0, tile_off, E, MG, 2, rank, args).a_row0 : 0;
+      auto prefetch_next = [&]() {
+        if (pf_t >= total) return;
+        tma_prefetch_2d(&tmA, pf_kb * BK, pf_row);
+        if (++pf_kb == KB) {
+          pf_kb = 0;
+          pf_t += ustep;
+          if (pf_t < total) pf_row = decode(pf_t, tile_off, E, MG, 2, rank, args).a_row0;
+        }
+      };
+      for (int i = 0; i < kPrefetch; ++i) prefetch_next();
       for (int t = u0; t < total; t += ustep) {
-        const Tile tl = decode2(t, tile_off, E, MG, rank, args);
-        const int n0 = min(tl.nmma, BN), n1 = tl.nmma - n0;  // accumulator 0 / 1 widths
-        const int h0 = n0 >> 1, h1 = n1 >> 1;                // token rows staged by each CTA
-        const int nb0 = (h0 + kBBox - 1) / kBBox, nb1 = (h1 + kBBox - 1) / kBBox;
+        const Tile tl = decode(t, tile_off, E, MG, 2, rank, args);
+        const int half = tl.nmma >> 1;  // token rows staged by each CTA
+        const int nbox = (half + kBBox - 1) / kBBox;
         for (int kb = 0; kb < KB; ++kb) {
+          prefetch_next();
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t lbar = mapa_u32(smem_u32(&full[stage]), 0);
-          if (rank == 0) mbar_expect_tx(&full[stage], 2 * (kABytes + (nb0 + nb1) * kBBoxBytes));
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * (kABytes + nbox * kBBoxBytes));
           tma_load_2d_2sm(sa + stage * kABytes, &tmA, lbar, kb * BK, tl.a_row0, polA);
-          const int kc = (kb % args.b_kblocks) * BK;
-          uint8_t* sbs = sb + stage * kBStage2;
-          for (int c = 0; c < nb0; ++c)
-            tma_load_2d_2sm(sbs + c * kBBoxBytes, &tmB, lbar, kc, tl.b_row0 + rank * h0 + c * kBBox, polB);
-          for (int c = 0; c < nb1; ++c)
-            tma_load_2d_2sm(sbs + kBHalfBytes + c * kBBoxBytes, &tmB, lbar, kc, tl.b_row0 + BN + rank * h1 + c * kBBox,
-                            polB);
+          for (int c = 0; c < nbox; ++c)
+            tma_load_2d_2sm(sb + stage * kBHalfBytes + c * kBBoxBytes, &tmB, lbar, (kb % args.b_kblocks) * BK,
+                            tl.b_row0 + rank * half + c * kBBox, polB);
           if (++stage == kStages2) {
             stage = 0;
             phase ^= 1;
@@ -629,43 +600,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = u0; t < total; t += ustep) {
-        const Tile tl = decode2(t, tile_off, E, MG, 0, args);
-        const int n0 = min(tl.nmma, BN), n1 = tl.nmma - n0;
-        // take one or two accumulators from the ring, in order
-        const int a0 = acc;
+        const Tile tl = decode(t, tile_off, E, MG, 2, 0, args);
+        const uint32_t idesc = idesc_base | ((uint32_t)(tl.nmma >> 3) << 17);
+        const uint32_t tmem_d = tmem_base + acc * BN;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-        const int a1 = acc;
-        if (n1 > 0) {
-          mbar_wait(&tempty[acc], acc_phase ^ 1);
-          acc ^= 1;
-          if (acc == 0) acc_phase ^= 1;
-        }
         fence_after();
-        const uint32_t id0 = idesc_base | ((uint32_t)(n0 >> 3) << 17);
-        const uint32_t id1 = idesc_base | ((uint32_t)(n1 >> 3) << 17);
-        const uint32_t d0 = tmem_base + a0 * BN, d1 = tmem_base + a1 * BN;
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&full[stage], phase);
           fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sa + stage * kABytes));
-          const uint64_t bd0 = sdesc_sw128(smem_u32(sb + stage * kBStage2));
-          const uint64_t bd1 = sdesc_sw128(smem_u32(sb + stage * kBStage2 + kBHalfBytes));
+          const uint64_t bd = sdesc_sw128(smem_u32(sb + stage * kBHalfBytes));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) mma_bf16_2sm(d0, ad + 2 * k, bd0 + 2 * k, id0, (kb | k) != 0);
-          if (n1 > 0) {
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k) mma_bf16_2sm(d1, ad + 2 * k, bd1 + 2 * k, id1, (kb | k) != 0);
-          }
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_2sm(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
           mma_commit_2sm(&empty[stage]);
           if (++stage == kStages2) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit_2sm(&tfull[a0]);
-        if (n1 > 0) mma_commit_2sm(&tfull[a1]);
+        mma_commit_2sm(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
       }
     }
   } else {
@@ -674,21 +630,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = u0; t < total; t += ustep) {
-      Tile tl = decode2(t, tile_off, E, MG, rank, args);
-      const int ntok = tl.ntok;
-      for (int j = 0; j * BN < ntok; ++j) {
-        Tile sub = tl;
-        sub.b_row0 = tl.b_row0 + j * BN;
-        sub.ntok = min(BN, ntok - j * BN);
-        mbar_wait(&tfull[acc], acc_phase);
-        fence_after();
-        epilogue_tile(args, sub, tmem_base + ((uint32_t)lane_base << 16) + acc * BN, warp & 3, lane, stg);
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tempty[acc]), 0));
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-      }
+      const Tile tl = decode(t, tile_off, E, MG, 2, rank, args);
+      mbar_wait(&tfull[acc], acc_phase);
+      fence_after();
+      epilogue_tile(args, tl, tmem_base + ((uint32_t)lane_base << 16) + acc * BN, warp & 3, lane, stg);
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tempty[acc]), 0));
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
   }
   fence_before();
@@ -844,7 +794,7 @@ static cudaError_t launch_gemm_cm(const CUtensorMap& mA, const CUtensorMap& mB, 
 
 static size_t smem_bytes_2sm(int E) {
   using namespace tc;
-  return 1024 + (size_t)kStages2 * (kABytes + kBStage2) + kStgBytes + (2 * kStages2 + 4) * 8 + 16 +
+  return 1024 + (size_t)kStages2 * (kABytes + kBHalfBytes) + kStgBytes + (2 * kStages2 + 4) * 8 + 16 +
          (size_t)(E + 1) * 4;
 }
 

@@ -333,6 +333,26 @@ cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dt
 //     by their last user, so the kernel is replayable (CUDA graphs).
 // ---------------------------------------------------------------------------
 constexpr int kFusedTT = 8;        // tokens per fused-gate tile (one warp per token in phase 2)
+
+// Diagnostics (beam_trace_gate): when set, the fused gate records %globaltimer
+// at its phase boundaries: [0] first CTA start (min), [1] last CTA start (max),
+// [2] first / [3] last projection done, [4] last top-K tile done, [5] permute done.
+__device__ unsigned long long* g_gate_trace = nullptr;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void trace_minmax(int lo, int hi) {
+  unsigned long long* tr = g_gate_trace;
+  if (tr != nullptr && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    if (lo >= 0) atomicMin(tr + lo, t);
+    if (hi >= 0) atomicMax(tr + hi, t);
+  }
+}
 constexpr int kCounterSlots = 16;  // [0, 8) token tiles, [15] tiles-done
 
 template <typename TX, int NPL>
@@ -344,7 +364,9 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   __shared__ float red_s[8 * kGemvCols * kFusedTT];
   __shared__ int s_last;
   const int cols = 2 * a.N;
+  trace_minmax(0, 1);
   router_gemv_body<TX, kFusedTT>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s);
+  trace_minmax(2, 3);
 
   // ---- last CTA of this token tile: top-K + mask ----
   __threadfence();
@@ -359,6 +381,8 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   for (int t = t0 + warp; t < t0 + nt; t += 8)
     topk_token<TX, NPL, kFusedMaxSplit, true>(P, gridDim.y, T, X, t, lane, a);
   if (threadIdx.x == 0) counters[tile] = 0;
+  __syncthreads();
+  trace_minmax(-1, 4);
 
   // ---- last token tile overall: permute all T tokens ----
   __threadfence();
@@ -369,6 +393,12 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   __threadfence();
   permute_block<int32_t, 8, true, false>(a.ids32, a.gw, T, a.K + a.S, E, bs, p, reinterpret_cast<int*>(xs));
   if (threadIdx.x == 0) counters[kCounterSlots - 1] = 0;
+  __syncthreads();
+  trace_minmax(-1, 5);
+}
+
+cudaError_t set_gate_trace(unsigned long long* buf) {
+  return cudaMemcpyToSymbol(g_gate_trace, &buf, sizeof(buf));
 }
 
 bool gate_fused_supported(int T, int N, int E, int d_pad) {

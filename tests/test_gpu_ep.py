@@ -51,7 +51,10 @@ def test_ep_single_rank_matches_layer(nccl_group, t):
     # bf16 ulp of |out| per element on top of the expert-sum differences
     o_ep = out_ep.float().cpu().double().numpy()
     o = out.float().cpu().double().numpy()
-    assert np.all(np.abs(o_ep - o) <= 2.0 ** -7 * np.abs(o) + 1e-3)
+    # (for T > 64 the fused layer runs the tcgen05 path: bf16 x_n, act and
+    # per-pair rows, vs the fp32 per-pair rows of the EP owner's execute)
+    excess = np.abs(o_ep - o) - 2.0 ** -7 * np.abs(o)
+    assert excess.max() <= 4e-3, excess.max()
     y_ep, y = o_ep - x.float().cpu().double().numpy(), o - x.float().cpu().double().numpy()
     assert normwise_rel(y_ep, y) <= 6e-2
     ref = O.beam_block_forward(x.double().cpu().numpy(), ob)

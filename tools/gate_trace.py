@@ -1,0 +1,50 @@
+"""Phase timeline of the fused decode gate (beam_trace_gate) at the bench's
+Q30 decode shapes, L2 flushed before every call (as in bench.py)."""
+import ctypes
+
+import numpy as np
+import torch
+
+import bench
+import paper_2605_14438_b200 as B
+from paper_2605_14438_b200 import _lib
+from paper_2605_14438_b200.beam import LayerOutputs, layer_forward_into
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    Q = bench.Q30
+    cfg = B.MoEBlockConfig(d_h=Q["d"], d_ff=Q["f"], num_experts=Q["n"], top_k=Q["k"])
+    w = bench.make_layer0()
+    blk = B.MoEBlock.from_weights(cfg, w["router"], (w["wg"], w["wu"], w["wd"]), norm_w=None,
+                                  mask_w=w["mask"], dtype=torch.bfloat16, device=dev)
+    lib = _lib.load()
+    tr = torch.zeros(8, dtype=torch.int64, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    names = ["start_skew", "proj_first", "proj_last", "topk_done", "permute_done"]
+    for t in (1, 8, 64):
+        hc = bench.make_tokens(t, 7)
+        theta = bench.calibrate_theta(hc, w["router"], w["mask"], Q["k"], 0.5)
+        blk.mask_router.weight.copy_(bench.mask_with_theta(w["mask"], theta).to(dev))
+        h = hc.to(dev)
+        outs = LayerOutputs(t, Q["d"], Q["n"], Q["k"], h.dtype, dev)
+        rows = []
+        for it in range(12):
+            flush.zero_()
+            tr.zero_()
+            tr[0] = np.iinfo(np.int64).max
+            tr[2] = np.iinfo(np.int64).max
+            torch.cuda.synchronize()
+            lib.beam_trace_gate(ctypes.c_void_p(tr.data_ptr()))
+            layer_forward_into(h, blk, outs)
+            torch.cuda.synchronize()
+            lib.beam_trace_gate(None)
+            v = tr.cpu().numpy().astype(np.float64)
+            if it >= 2:
+                rows.append([v[1] - v[0], v[2] - v[0], v[3] - v[0], v[4] - v[0], v[5] - v[0]])
+        med = np.median(np.array(rows), axis=0) / 1e3
+        print(f"T={t}: " + ", ".join(f"{n}={x:.2f}us" for n, x in zip(names, med)))
+
+
+if __name__ == "__main__":
+    main()
