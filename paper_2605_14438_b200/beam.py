@@ -17,6 +17,7 @@ front.  ``mask_forward`` alone honours any tau via a >= logit(tau).
 from __future__ import annotations
 
 import ctypes
+import functools
 import math
 from dataclasses import dataclass
 
@@ -98,36 +99,57 @@ def rms_norm(h, weight, eps: float = 1e-6) -> torch.Tensor:
 # ---------------------------------------------------------------------------
 
 
+@functools.lru_cache(maxsize=256)
+def _outputs_layout(t: int, d: int, n: int, k: int, out_dtype: torch.dtype):
+    """(total bytes, ((name, byte offset, shape, dtype), ...)) of one layer's
+    outputs in a single flat buffer (256-byte aligned fields)."""
+    es = torch.empty(0, dtype=out_dtype).element_size()
+    spec = [("out", (t, d), out_dtype, es), ("topk_ids", (t, k), torch.int64, 8),
+            ("masked_ids", (t, k), torch.int64, 8)]
+    spec += [(name, (t, n), torch.float32, 4)
+             for name in ("logits", "weights", "pre_activation", "raw_mask", "mask")]
+    fields, off = [], 0
+    for name, shape, dt, size in spec:
+        off = (off + 255) // 256 * 256
+        fields.append((name, off, shape, dt))
+        off += int(np.prod(shape)) * size
+    return off, tuple(fields)
+
+
 class LayerOutputs:
     """All outputs of one layer call carved from ONE flat buffer, so a host
-    caller pays a single device->host copy."""
+    caller pays a single device->host copy.  Views are created on first use
+    (a device-side staging copy never builds any)."""
 
     def __init__(self, t: int, d: int, n: int, k: int, out_dtype: torch.dtype, device, pin=False):
-        es = torch.empty(0, dtype=out_dtype).element_size()
-        spec = [("out", (t, d), out_dtype, es), ("topk_ids", (t, k), torch.int64, 8),
-                ("masked_ids", (t, k), torch.int64, 8)]
-        spec += [(name, (t, n), torch.float32, 4)
-                 for name in ("logits", "weights", "pre_activation", "raw_mask", "mask")]
-        offs, off = [], 0
-        for name, shape, dt, size in spec:
-            off = (off + 255) // 256 * 256
-            offs.append(off)
-            off += int(np.prod(shape)) * size
-        self.nbytes = off
+        self.nbytes, self._fields = _outputs_layout(t, d, n, k, out_dtype)
         kw = dict(dtype=torch.uint8, device=device)
-        self.buf = torch.empty(off, pin_memory=pin, **kw) if pin else torch.empty(off, **kw)
-        self.views = {}
-        for (name, shape, dt, size), o in zip(spec, offs):
-            n_el = int(np.prod(shape))
-            self.views[name] = self.buf[o : o + n_el * size].view(dt).view(shape)
+        self.buf = torch.empty(self.nbytes, pin_memory=pin, **kw) if pin else torch.empty(self.nbytes, **kw)
+        self._views = {}
 
     def __getitem__(self, name):
-        return self.views[name]
+        v = self._views.get(name)
+        if v is None:
+            for fname, off, shape, dt in self._fields:
+                if fname == name:
+                    size = torch.empty(0, dtype=dt).element_size()
+                    n_el = int(np.prod(shape))
+                    v = self.buf[off : off + n_el * size].view(dt).view(shape)
+                    self._views[name] = v
+                    break
+            else:
+                raise KeyError(name)
+        return v
+
+    @property
+    def views(self):
+        return {fname: self[fname] for fname, _, _, _ in self._fields}
 
     def ctypes_outputs(self) -> _lib.Outputs:
         o = _lib.Outputs()
-        for name, v in self.views.items():
-            setattr(o, name, v.data_ptr())
+        base = self.buf.data_ptr()
+        for name, off, _, _ in self._fields:
+            setattr(o, name, base + off)
         return o
 
     def copy_from(self, other: "LayerOutputs") -> None:

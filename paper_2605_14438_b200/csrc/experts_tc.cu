@@ -178,7 +178,8 @@ __device__ __forceinline__ Tile decode(int u, const int* tile_off, int E, int MG
 
 constexpr int kStgBytes = 32 * BM * 4;  // epilogue staging: 32 tokens x 128 rows (fp32 worst case)
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// named barrier over the 4 epilogue warps of one group (ids 1, 2)
+__device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 
 // One accumulator tile -> global, 32 token columns at a time.  The 4 epilogue
 // warps (TMEM lanes 32*w4..) transpose through shared memory so every global
@@ -187,10 +188,11 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 //   mode 0: act[pos, f]   = bf16(silu(gate) * up)  (64 features per tile)
 //   mode 1: opair[pos, d] = bf16(ghat[pos] * acc)  (128 output channels)
 //   mode 2: P[t, c]       = acc (fp32, router / mask logits)
+// A group of 4 epilogue warps (one per TMEM lane quadrant, barrier `bar`) takes
+// the 32-token chunks c_begin, c_begin + c_step, ...
 __device__ __forceinline__ void epilogue_tile(const Args& args, const Tile& tl, uint32_t tbase, int w4, int lane,
-                                              uint8_t* stg) {
-  const int ew = threadIdx.x - 64;  // 0..127 within the epilogue warps
-  for (int c0 = 0; c0 < tl.ntok; c0 += 32) {
+                                              uint8_t* stg, int c_begin = 0, int c_step = 32, int bar = 1) {
+  for (int c0 = c_begin; c0 < tl.ntok; c0 += c_step) {
     const int rows = min(32, tl.ntok - c0);
     float v[32];
     tmem_ld32(tbase + c0, v);
@@ -207,7 +209,7 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const Tile& tl, 
         const float u = lo ? r : v[16 + j];
         s[(lo ? j : 16 + j) * 64 + fl] = __float2bfloat16_rn(activation<BEAM_ACT_SILU>(g) * u);
       }
-      epi_bar();
+      epi_bar(bar);
       for (int row = w4; row < rows; row += 4) {
         const uint32_t val = reinterpret_cast<const uint32_t*>(s + row * 64)[lane];
         reinterpret_cast<uint32_t*>(args.act + (size_t)(tl.b_row0 + c0 + row) * args.f_pad + tl.m_tile * 64)[lane] = val;
@@ -220,7 +222,7 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const Tile& tl, 
         const float wj = __shfl_sync(0xffffffffu, wl, j);
         s[j * BM + 32 * w4 + lane] = __float2bfloat16_rn(v[j] * wj);
       }
-      epi_bar();
+      epi_bar(bar);
       for (int row = w4; row < rows; row += 4) {
         const uint2 val = reinterpret_cast<const uint2*>(s + row * BM)[lane];
         reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(args.opair) + (size_t)(tl.b_row0 + c0 + row) * args.d_pad +
@@ -230,16 +232,15 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const Tile& tl, 
       float* s = reinterpret_cast<float*>(stg);  // [32 tokens][128 columns]
 #pragma unroll
       for (int j = 0; j < 32; ++j) s[j * BM + 32 * w4 + lane] = v[j];
-      epi_bar();
+      epi_bar(bar);
       for (int row = w4; row < rows; row += 4) {
         const float4 val = reinterpret_cast<const float4*>(s + row * BM)[lane];
         reinterpret_cast<float4*>(reinterpret_cast<float*>(args.opair) + (size_t)(tl.b_row0 + c0 + row) * args.m_rows +
                                   tl.m_tile * BM)[lane] = val;
       }
     }
-    epi_bar();  // staging reused by the next chunk
+    epi_bar(bar);  // staging reused by the next chunk
   }
-  (void)ew;
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // signal the leader's full barrier; the leader's commits release both CTAs'
 // stages (multicast); both epilogues release the leader's accumulator barrier.
 // ---------------------------------------------------------------------------
-constexpr int kStages2 = 6;
+constexpr int kStages2 = 5;
 constexpr int kBHalfBytes = (BN / 2) * BK * 2;  // 16 KB: 128 token rows
 
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
@@ -457,16 +458,6 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       : "memory");
 }
 
-// Weight tile -> L2 only (no smem, no barrier): issued kPrefetch k-blocks ahead of
-// the staged loads so the HBM latency of the weight stream is not bounded by the
-// smem ring depth.
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
-constexpr int kPrefetch = 16;
 
 __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                              uint32_t accumulate) {
@@ -488,15 +479,17 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+constexpr int kThreads2 = 320;  // producer, MMA, 2 x 4 epilogue warps
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                             Args args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;                                  // kStages2 x 16 KB (this CTA's 128 weight rows)
   uint8_t* sb = smem + kStages2 * kABytes;             // kStages2 x 16 KB (this CTA's half of the tokens)
-  uint8_t* stg = sb + kStages2 * kBHalfBytes;          // epilogue staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(stg + kStgBytes);
+  uint8_t* stg = sb + kStages2 * kBHalfBytes;          // epilogue staging, one per epilogue group
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + 2 * kStgBytes);
   uint64_t* empty = full + kStages2;
   uint64_t* tfull = empty + kStages2;
   uint64_t* tempty = tfull + 2;
@@ -532,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (used on the leader)
+      mbar_init(&tempty[b], 16);  // 8 epilogue warps x 2 CTAs (used on the leader)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -559,24 +552,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t polA = l2_policy(args.mode != 2), polB = l2_policy(false);
       int stage = 0;
       uint32_t phase = 0;
-      // L2 prefetch cursor for this CTA's weight rows, kPrefetch k-blocks ahead
-      int pf_t = u0, pf_kb = 0, pf_row = u0 < total ? decode(u0, tile_off, E, MG, 2, rank, args).a_row0 : 0;
-      auto prefetch_next = [&]() {
-        if (pf_t >= total) return;
-        tma_prefetch_2d(&tmA, pf_kb * BK, pf_row);
-        if (++pf_kb == KB) {
-          pf_kb = 0;
-          pf_t += ustep;
-          if (pf_t < total) pf_row = decode(pf_t, tile_off, E, MG, 2, rank, args).a_row0;
-        }
-      };
-      for (int i = 0; i < kPrefetch; ++i) prefetch_next();
       for (int t = u0; t < total; t += ustep) {
         const Tile tl = decode(t, tile_off, E, MG, 2, rank, args);
         const int half = tl.nmma >> 1;  // token rows staged by each CTA
         const int nbox = (half + kBBox - 1) / kBBox;
         for (int kb = 0; kb < KB; ++kb) {
-          prefetch_next();
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t lbar = mapa_u32(smem_u32(&full[stage]), 0);
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * (kABytes + nbox * kBBoxBytes));
@@ -626,14 +606,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------- epilogue (both CTAs: own TMEM = own 128 rows) ----------------
+    // warps 2-5 and 6-9: two groups covering the 4 TMEM lane quadrants each,
+    // alternating 32-token chunks
     const int lane_base = 32 * (warp & 3);
+    const int grp = (warp - 2) >> 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = u0; t < total; t += ustep) {
       const Tile tl = decode(t, tile_off, E, MG, 2, rank, args);
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
-      epilogue_tile(args, tl, tmem_base + ((uint32_t)lane_base << 16) + acc * BN, warp & 3, lane, stg);
+      epilogue_tile(args, tl, tmem_base + ((uint32_t)lane_base << 16) + acc * BN, warp & 3, lane,
+                    stg + grp * kStgBytes, 32 * grp, 64, 1 + grp);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(&tempty[acc]), 0));
@@ -794,7 +778,7 @@ static cudaError_t launch_gemm_cm(const CUtensorMap& mA, const CUtensorMap& mB, 
 
 static size_t smem_bytes_2sm(int E) {
   using namespace tc;
-  return 1024 + (size_t)kStages2 * (kABytes + kBHalfBytes) + kStgBytes + (2 * kStages2 + 4) * 8 + 16 +
+  return 1024 + (size_t)kStages2 * (kABytes + kBHalfBytes) + 2 * kStgBytes + (2 * kStages2 + 4) * 8 + 16 +
          (size_t)(E + 1) * 4;
 }
 
@@ -808,7 +792,7 @@ static cudaError_t launch_gemm_2sm(const CUtensorMap& mA, const CUtensorMap& mB,
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((num_sms() / 2) * 2);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kThreads2);
   cfg.dynamicSmemBytes = smem_bytes_2sm(a.E);
   cfg.stream = s;
   cudaLaunchAttribute at[1];

@@ -335,6 +335,10 @@ class MoEBlock:
             else:
                 gate[cfg.num_experts :].zero_()
             self._pack_key = key
+        ck = (key, mask_threshold, id(self.norm_w), id(self.w_gu), id(self.w_down), id(self.gate_wT))
+        cached = getattr(self, "_desc_cache", None)
+        if cached is not None and cached[0] == ck:
+            return cached[1]
         d = _lib.LayerDesc()
         d.d_h, d.d_ff, d.num_experts, d.top_k = cfg.d_h, cfg.d_ff, cfg.num_experts, cfg.top_k
         d.num_shared = cfg.num_shared
@@ -346,6 +350,7 @@ class MoEBlock:
         d.gate_wT = self.gate_wT.data_ptr()
         d.w_gu = self.w_gu.data_ptr()
         d.w_down = self.w_down.data_ptr()
+        self._desc_cache = (ck, d)
         return d
 
     def weight_bytes(self) -> int:

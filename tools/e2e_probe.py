@@ -2,8 +2,13 @@
 into its pieces at the bench headline workload (Q30, T=64, s=0.5)."""
 import time
 
+import os
+import sys
+
 import numpy as np
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2605_14438_b200 as B
 from paper_2605_14438_b200.beam import LayerOutputs, layer_forward_into

@@ -5,6 +5,8 @@ import ctypes
 import numpy as np
 import torch
 
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
 import paper_2605_14438_b200 as B
 from paper_2605_14438_b200 import _lib
