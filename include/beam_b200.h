@@ -160,10 +160,10 @@ unsigned long long beam_kernel_launches(void);
 int beam_set_expert_path(int mode);
 int beam_profile_begin(int max_calls);
 int beam_profile_end(float* stage_ms, int* calls);
-/* Fused decode gate phase timestamps (%globaltimer ns) into a device buffer of 6
+/* Fused decode gate phase timestamps (%globaltimer ns) into a device buffer of 8
  * u64 (caller initialises [0],[2] to ~0 and the rest to 0); NULL disables:
  * {first CTA start, last CTA start, first / last projection done,
- *  last top-K tile done, permute done}. */
+ *  last top-K tile done, permute done, last top-K tile start, permute start}. */
 int beam_trace_gate(unsigned long long* dev_buf);
 const char* beam_last_cuda_error(void);
 const char* beam_build_info(void);

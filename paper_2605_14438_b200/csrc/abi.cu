@@ -1,6 +1,7 @@
 // C ABI entry points (include/beam_b200.h): argument validation, workspace
 // carving and the launch sequence of each reference-facing operation.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -154,10 +155,29 @@ static int validate(const beam_layer_t* L) {
 
 static int status(cudaError_t e) { return record(e) == cudaSuccess ? BEAM_OK : BEAM_ERR_CUDA; }
 
-#define BEAM_TRY(expr)                          \
-  do {                                          \
-    cudaError_t _e = (expr);                    \
-    if (_e != cudaSuccess) return status(_e);   \
+// BEAM_DEBUG_SYNC=1: synchronise after every stage and name the failing one in
+// beam_last_cuda_error (diagnostics for asynchronous kernel faults).
+static bool debug_sync() {
+  static const bool on = [] {
+    const char* v = getenv("BEAM_DEBUG_SYNC");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+static int status_at(cudaError_t e, const char* what) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what, cudaGetErrorString(e));
+  return BEAM_ERR_CUDA;
+}
+
+#define BEAM_TRY(expr)                                           \
+  do {                                                           \
+    cudaError_t _e = (expr);                                     \
+    if (_e != cudaSuccess) return status(_e);                    \
+    if (debug_sync()) {                                          \
+      _e = cudaDeviceSynchronize();                              \
+      if (_e != cudaSuccess) return status_at(_e, #expr);        \
+    }                                                            \
   } while (0)
 
 }  // namespace beam

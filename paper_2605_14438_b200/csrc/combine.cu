@@ -21,6 +21,12 @@ namespace beam {
 
 constexpr int kCombineWarps = 8;
 
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const uint32_t a = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+  const uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
+  return a | (b << 16);
+}
+
 template <typename TP>
 __device__ __forceinline__ void ld_pair8(const TP* p, float* v) {
   if constexpr (sizeof(TP) == 2) {
@@ -36,7 +42,7 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const int32
                                                                      const int32_t* __restrict__ slot_pos,
                                                                      const TP* __restrict__ opair, int T, int Keff,
                                                                      int d, int d_pad, const TH* __restrict__ h,
-                                                                     TO* __restrict__ out) {
+                                                                     TO* __restrict__ out, bool vec) {
   griddep_wait();
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * kCombineWarps + (threadIdx.x >> 5);
@@ -65,9 +71,19 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const int32
   }
   {
     const int c0 = blockIdx.y * 256 + 8 * lane;
-    float y[8];
+    float y[8], hv[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) y[q] = 0.0f;
+    const bool vrow = vec && c0 + 8 <= d;
+    if (vrow && h != nullptr) {  // residual row issued before the pair rows (latency overlap)
+      const uint4* hp = reinterpret_cast<const uint4*>(h + (size_t)t * d + c0);
+      if constexpr (sizeof(TH) == 2) {
+        unpack<__nv_bfloat16>(__ldg(hp), hv);
+      } else {
+        unpack<float>(__ldg(hp), hv);
+        unpack<float>(__ldg(hp + 1), hv + 4);
+      }
+    }
     for (int r0 = 0; r0 < nv; r0 += 8) {
       float v[8][8];
 #pragma unroll
@@ -82,13 +98,33 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const int32
           for (int i = 0; i < 8; ++i) y[i] += v[q][i];
         }
     }
+    if (vrow) {
+      // 16-byte row loads / stores (d % 8 == 0 and 16-byte aligned rows)
+      if (h != nullptr) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int c = c0 + i;
-      if (c < d) {
-        float o = y[i];
-        if (h != nullptr) o = to_f32<TH>(h[(size_t)t * d + c]) + o;
-        out[(size_t)t * d + c] = from_f32<TO>(o);
+        for (int i = 0; i < 8; ++i) y[i] = hv[i] + y[i];
+      }
+      uint4* op = reinterpret_cast<uint4*>(out + (size_t)t * d + c0);
+      if constexpr (sizeof(TO) == 2) {
+        uint4 o;
+        o.x = pack_bf16x2(y[0], y[1]);
+        o.y = pack_bf16x2(y[2], y[3]);
+        o.z = pack_bf16x2(y[4], y[5]);
+        o.w = pack_bf16x2(y[6], y[7]);
+        *op = o;
+      } else {
+        op[0] = make_uint4(__float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]), __float_as_uint(y[3]));
+        op[1] = make_uint4(__float_as_uint(y[4]), __float_as_uint(y[5]), __float_as_uint(y[6]), __float_as_uint(y[7]));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = c0 + i;
+        if (c < d) {
+          float o = y[i];
+          if (h != nullptr) o = to_f32<TH>(h[(size_t)t * d + c]) + o;
+          out[(size_t)t * d + c] = from_f32<TO>(o);
+        }
       }
     }
   }
@@ -97,15 +133,16 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const int32
 template <typename TP>
 static cudaError_t combine_dispatch(const PlanDev& p, const TP* opair, int T, int Keff, int d, int d_pad,
                                     const void* h, int h_dtype, void* out, int out_dtype, cudaStream_t s) {
+  const bool vec = d % 8 == 0 && (reinterpret_cast<uintptr_t>(h) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   const dim3 grid(ceil_div(T, kCombineWarps), ceil_div(d, 256));
   const int thr = 32 * kCombineWarps;
   if (out_dtype == BEAM_F32 && h_dtype == BEAM_F32)
-    return launch_pdl(combine_kernel<float, float, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const float*)h, (float*)out);
+    return launch_pdl(combine_kernel<float, float, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const float*)h, (float*)out, vec);
   if (out_dtype == BEAM_BF16 && h_dtype == BEAM_BF16)
-    return launch_pdl(combine_kernel<__nv_bfloat16, __nv_bfloat16, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const __nv_bfloat16*)h, (__nv_bfloat16*)out);
+    return launch_pdl(combine_kernel<__nv_bfloat16, __nv_bfloat16, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const __nv_bfloat16*)h, (__nv_bfloat16*)out, vec);
   if (out_dtype == BEAM_F32)
-    return launch_pdl(combine_kernel<__nv_bfloat16, float, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const __nv_bfloat16*)h, (float*)out);
-  return launch_pdl(combine_kernel<float, __nv_bfloat16, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const float*)h, (__nv_bfloat16*)out);
+    return launch_pdl(combine_kernel<__nv_bfloat16, float, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const __nv_bfloat16*)h, (float*)out, vec);
+  return launch_pdl(combine_kernel<float, __nv_bfloat16, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const float*)h, (__nv_bfloat16*)out, vec);
 }
 
 cudaError_t launch_combine(const PlanDev& p, const void* opair, int opair_dtype, int T, int Keff, int d, int d_pad,

@@ -24,6 +24,8 @@
 //     fp32 opair[pos, d] for the deterministic ascending-expert combine.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "beam_common.cuh"
 #include "beam_internal.h"
 
@@ -55,6 +57,7 @@ struct Args {
   int f_pad;
   void* opair;  // mode 1: [cap, d_pad] bf16 per-pair rows; mode 2: fp32 logits
   int d_pad;
+  int bn;  // token-tile width (<= BN, multiple of 16): narrower tiles spread few-expert GEMMs over more SMs
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -169,8 +172,8 @@ __device__ __forceinline__ Tile decode(int u, const int* tile_off, int E, int MG
   r.m_tile = (local / nt) * CM + rank;
   const int n_tile = local % nt;
   r.a_row0 = lo * a.m_rows + r.m_tile * BM;
-  const int tok0 = n_tile * BN;
-  r.ntok = min(BN, a.counts[lo] - tok0);
+  const int tok0 = n_tile * a.bn;
+  r.ntok = min(a.bn, a.counts[lo] - tok0);
   r.b_row0 = a.offsets[lo] + tok0;
   r.nmma = (r.ntok + 15) & ~15;
   return r;
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) tile_off[0] = 0;
     for (int base = 0; base < E; base += 32) {
       const int e = base + lane;
-      int v = e < E ? (args.counts[e] + BN - 1) / BN : 0;
+      int v = e < E ? (args.counts[e] + args.bn - 1) / args.bn : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, v, o);
@@ -508,7 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     if (lane == 0) tile_off[0] = 0;
     for (int base = 0; base < E; base += 32) {
       const int e = base + lane;
-      int v = e < E ? (args.counts[e] + BN - 1) / BN : 0;
+      int v = e < E ? (args.counts[e] + args.bn - 1) / args.bn : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, v, o);
@@ -827,10 +830,10 @@ cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* 
       !make_map(&mB2, act16, (uint64_t)cap, g.f_pad, kBBox))
     return cudaErrorInvalidValue;
   const size_t smem = smem_bytes(g.E);
-  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
+  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN};
   cudaError_t e = launch_gemm(mA1, mB1, a1, smem, true, s);
   if (e != cudaSuccess) return e;
-  Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad};
+  Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN};
   return launch_gemm(mA2, mB2, a2, smem, true, s);
 }
 
@@ -881,7 +884,13 @@ cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* ga
   CUtensorMap mA, mB;
   if (!make_map(&mA, A3, (uint64_t)cols, 3ull * d_pad, BM) || !make_map(&mB, X, (uint64_t)T, d_pad, kBBox))
     return cudaErrorInvalidValue;
-  Args a{2, 1, cols, 3 * d_pad, d_pad / BK, plan1, plan1 + 1, nullptr, nullptr, 0, P, 0};
+  // one "expert" of T tokens: narrow the token tiles until the units cover the SMs
+  static const int env_bn = [] {
+    const char* v = getenv("BEAM_ROUTER_BN");  // tuning knob
+    return v ? atoi(v) : 0;
+  }();
+  int bn = env_bn >= 16 && env_bn <= BN && env_bn % 16 == 0 ? env_bn : BN;
+  Args a{2, 1, cols, 3 * d_pad, d_pad / BK, plan1, plan1 + 1, nullptr, nullptr, 0, P, 0, bn};
   return launch_gemm(mA, mB, a, smem_bytes(1), true, s);
 }
 

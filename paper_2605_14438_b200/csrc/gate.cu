@@ -336,7 +336,8 @@ constexpr int kFusedTT = 8;        // tokens per fused-gate tile (one warp per t
 
 // Diagnostics (beam_trace_gate): when set, the fused gate records %globaltimer
 // at its phase boundaries: [0] first CTA start (min), [1] last CTA start (max),
-// [2] first / [3] last projection done, [4] last top-K tile done, [5] permute done.
+// [2] first / [3] last projection done, [6] last top-K tile start, [4] last top-K
+// tile done, [7] permute start, [5] permute done.
 __device__ unsigned long long* g_gate_trace = nullptr;
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  trace_minmax(-1, 6);
   const int t0 = tile * kFusedTT, nt = min(kFusedTT, T - t0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int t = t0 + warp; t < t0 + nt; t += 8)
@@ -391,6 +393,7 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  trace_minmax(-1, 7);
   permute_block<int32_t, 8, true, false>(a.ids32, a.gw, T, a.K + a.S, E, bs, p, reinterpret_cast<int*>(xs));
   if (threadIdx.x == 0) counters[kCounterSlots - 1] = 0;
   __syncthreads();
