@@ -155,6 +155,14 @@ static int validate(const beam_layer_t* L) {
 
 static int status(cudaError_t e) { return record(e) == cudaSuccess ? BEAM_OK : BEAM_ERR_CUDA; }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("BEAM_NO_PDL");
+    return !(v && v[0] == '1');
+  }();
+  return on;
+}
+
 // BEAM_DEBUG_SYNC=1: synchronise after every stage and name the failing one in
 // beam_last_cuda_error (diagnostics for asynchronous kernel faults).
 static bool debug_sync() {

@@ -62,6 +62,9 @@ cudaError_t record(cudaError_t e);
 // Launch with programmatic stream serialization (PDL) so the kernel's launch and
 // prologue overlap the previous kernel on the stream.  Kernels launched this way
 // call griddep_wait() before reading their predecessor's outputs.
+// Programmatic dependent launch on (default) / off (BEAM_NO_PDL=1, diagnostics).
+bool pdl_enabled();
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
@@ -74,7 +77,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 void count_launches(int n);  // bookkeeping for beam_kernel_launches()

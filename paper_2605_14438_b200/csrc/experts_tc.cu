@@ -814,6 +814,7 @@ static int g_gemm_variant = 0;
 static cudaError_t launch_gemm(const CUtensorMap& mA, const CUtensorMap& mB, const tc::Args& a, size_t smem,
                                bool pdl, cudaStream_t s) {
   const int mt = a.m_rows / tc::BM;
+  pdl = pdl && pdl_enabled();
   if (g_gemm_variant == 0 && mt % 2 == 0) return launch_gemm_2sm(mA, mB, a, pdl, s);
   return launch_gemm_cm<1>(mA, mB, a, smem, pdl, s);
 }
