@@ -13,7 +13,7 @@ from paper_2605_14438_b200 import _lib
 from paper_2605_14438_b200.beam import LayerOutputs, layer_forward_into
 
 
-def main():
+def main(flush_l2=True):
     dev = torch.device("cuda", 0)
     Q = bench.Q30
     cfg = B.MoEBlockConfig(d_h=Q["d"], d_ff=Q["f"], num_experts=Q["n"], top_k=Q["k"])
@@ -32,7 +32,8 @@ def main():
         outs = LayerOutputs(t, Q["d"], Q["n"], Q["k"], h.dtype, dev)
         rows = []
         for it in range(12):
-            flush.zero_()
+            if flush_l2:
+                flush.zero_()
             tr.zero_()
             tr[0] = np.iinfo(np.int64).max
             tr[2] = np.iinfo(np.int64).max
@@ -45,8 +46,9 @@ def main():
             if it >= 2:
                 rows.append([v[1] - v[0], v[2] - v[0], v[3] - v[0], v[6] - v[0], v[4] - v[0], v[7] - v[0], v[5] - v[0]])
         med = np.median(np.array(rows), axis=0) / 1e3
-        print(f"T={t}: " + ", ".join(f"{n}={x:.2f}us" for n, x in zip(names, med)))
+        print(f"T={t} flush={flush_l2}: " + ", ".join(f"{n}={x:.2f}us" for n, x in zip(names, med)))
 
 
 if __name__ == "__main__":
-    main()
+    main(True)
+    main(False)
