@@ -38,6 +38,7 @@ EXPORTS = (
     "beam_profile_begin",
     "beam_profile_end",
     "beam_trace_gate",
+    "beam_trace_decode",
     "beam_last_cuda_error",
     "beam_build_info",
 )
@@ -110,6 +111,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_profile_begin": (I, [I]),
         "beam_profile_end": (I, [P, P]),
         "beam_trace_gate": (I, [P]),
+        "beam_trace_decode": (I, [P]),
         "beam_last_cuda_error": (ctypes.c_char_p, []),
         "beam_build_info": (ctypes.c_char_p, []),
     }

@@ -252,10 +252,17 @@ int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, in
 
   prof_mark(0, s);
   BEAM_TRY(strided_input(g, h, h_dtype, T, w, &X, s));
+  if (!w.tc && g_expert_path.load() != 4 && decode_fused_supported(L, g, T)) {
+    // decode: the whole layer in one persistent kernel
+    BEAM_TRY(launch_decode_fused(L, g, X, h_dtype, T, topk_args(L, g, o, w), w.logits2, w.act,
+                                 reinterpret_cast<unsigned*>(w.counters + 32), o->out, s));
+    for (int m = 1; m < kStageMarks; ++m) prof_mark(m, s);
+    return BEAM_OK;
+  }
   if (gate_fused_supported(T, g.N, g.E, g.d_pad)) {
     // decode: projection + top-K + permute in one launch
     BEAM_TRY(launch_gate_fused(X, h_dtype, L.has_norm ? L.norm_w : nullptr, L.gate_wT, T, g.d, g.d_pad,
-                               w.logits2, topk_args(L, g, o, w), g.E, block_size, w.plan, w.counters, s));
+                               w.logits2, topk_args(L, g, o, w), g.E, block_size, w.tc, w.plan, w.counters, s));
     prof_mark(1, s);
   } else {
     BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s));
@@ -442,6 +449,8 @@ int beam_profile_end(float* stage_ms, int* calls) {
 }
 
 int beam_trace_gate(unsigned long long* dev_buf) { return status(beam::set_gate_trace(dev_buf)); }
+
+int beam_trace_decode(unsigned long long* dev_buf) { return status(beam::set_decode_trace(dev_buf)); }
 
 const char* beam_last_cuda_error(void) { return g_last_error; }
 

@@ -95,7 +95,7 @@ cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dt
 bool gate_fused_supported(int T, int N, int E, int d_pad);
 cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, const float* gate_wT, int T,
                               int d, int d_pad, float* P, const TopkArgs& a, int E, int bs,
-                              const PlanDev& p, int* counters, cudaStream_t s);
+                              bool pad, const PlanDev& p, int* counters, cudaStream_t s);
 cudaError_t launch_mask_route(const int64_t* ids, const void* a, int a_dtype, int T, int K,
                               int N, int64_t* out, cudaStream_t s);
 
@@ -158,11 +158,18 @@ cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* ga
 cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* xperm, const PlanDev& p,
                               int cap, void* act16, void* opair, cudaStream_t s);
 
+// decode_fused.cu (whole layer, T <= 64, one persistent cooperative kernel)
+bool decode_fused_supported(const beam_layer_t& L, const Dims& g, int T);
+cudaError_t launch_decode_fused(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
+                                const TopkArgs& tk, float* P, void* act, unsigned* bar, void* out,
+                                cudaStream_t s);
+
 // combine.cu
 cudaError_t launch_combine(const PlanDev& p, const void* opair, int opair_dtype, int T, int Keff, int d, int d_pad,
                            const void* h, int h_dtype, void* out, int out_dtype,
                            cudaStream_t s);
 
 cudaError_t set_gate_trace(unsigned long long* buf);
+cudaError_t set_decode_trace(unsigned long long* buf);
 
 }  // namespace beam

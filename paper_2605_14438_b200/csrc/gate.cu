@@ -360,7 +360,7 @@ template <typename TX, int NPL>
 __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ X, const float* __restrict__ nw,
                                                          const float* __restrict__ W, int T, int d, int d_pad,
                                                          int kr, float* __restrict__ P, TopkArgs a, int E,
-                                                         int bs, PlanDev p, int* __restrict__ counters) {
+                                                         int bs, bool pad, PlanDev p, int* __restrict__ counters) {
   extern __shared__ float xs[];  // phase 1: token tile; phase 3: permute scratch
   __shared__ float red_s[8 * kGemvCols * kFusedTT];
   __shared__ int s_last;
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   if (!s_last) return;
   __threadfence();
   trace_minmax(-1, 7);
-  permute_block<int32_t, 8, true, false>(a.ids32, a.gw, T, a.K + a.S, E, bs, p, reinterpret_cast<int*>(xs));
+  permute_block<int32_t, 8, true>(a.ids32, a.gw, T, a.K + a.S, E, bs, p, reinterpret_cast<int*>(xs), pad);
   if (threadIdx.x == 0) counters[kCounterSlots - 1] = 0;
   __syncthreads();
   trace_minmax(-1, 5);
@@ -411,19 +411,19 @@ bool gate_fused_supported(int T, int N, int E, int d_pad) {
 template <typename TX, int NPL>
 static cudaError_t fused_launch(dim3 grid, size_t smem, const void* X, const float* nw, const float* W, int T,
                                 int d, int d_pad, int kr, float* P, const TopkArgs& a, int E, int bs,
-                                const PlanDev& p, int* counters, cudaStream_t s) {
+                                bool pad, const PlanDev& p, int* counters, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     set_smem(gate_fused_kernel<TX, NPL>, 160 * 1024);
     attr = true;
   }
-  gate_fused_kernel<TX, NPL><<<grid, 256, smem, s>>>((const TX*)X, nw, W, T, d, d_pad, kr, P, a, E, bs, p, counters);
+  gate_fused_kernel<TX, NPL><<<grid, 256, smem, s>>>((const TX*)X, nw, W, T, d, d_pad, kr, P, a, E, bs, pad, p, counters);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, const float* gate_wT, int T,
                               int d, int d_pad, float* P, const TopkArgs& a, int E, int bs,
-                              const PlanDev& p, int* counters, cudaStream_t s) {
+                              bool pad, const PlanDev& p, int* counters, cudaStream_t s) {
   const int cols = 2 * a.N;
   const int kr = gemv_kr(T, cols, d_pad, kFusedMaxSplit, kFusedTT);
   dim3 grid(ceil_div(cols, 8 * kGemvCols), ceil_div(d_pad, kr), ceil_div(T, kFusedTT));
@@ -432,11 +432,11 @@ cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, c
   const int npl = ceil_div(a.N, 32);
   cudaError_t e;
 #define BEAM_FUSED(TX_)                                                                                        \
-  if (npl <= 1) e = fused_launch<TX_, 1>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, p, counters, s); \
-  else if (npl <= 2) e = fused_launch<TX_, 2>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, p, counters, s); \
-  else if (npl <= 4) e = fused_launch<TX_, 4>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, p, counters, s); \
-  else if (npl <= 8) e = fused_launch<TX_, 8>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, p, counters, s); \
-  else e = fused_launch<TX_, 16>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, p, counters, s);
+  if (npl <= 1) e = fused_launch<TX_, 1>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
+  else if (npl <= 2) e = fused_launch<TX_, 2>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
+  else if (npl <= 4) e = fused_launch<TX_, 4>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
+  else if (npl <= 8) e = fused_launch<TX_, 8>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
+  else e = fused_launch<TX_, 16>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s);
   if (x_dtype == BEAM_BF16) {
     BEAM_FUSED(__nv_bfloat16)
   } else {

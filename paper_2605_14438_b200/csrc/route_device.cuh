@@ -197,11 +197,13 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* scratch, int* to
 // bases (expert-major / warp-minor scan) -> ordered re-walk ranking equal experts
 // inside each 32-entry step with __match_any_sync.  Identical to the reference's
 // order (ascending flat index inside an expert) whatever the scheduling.
-// smem: NW*E + 2E + 1 + 32 ints.  PAD = write the -1 padding of every expert run
-// (the layer's own kernels never read it; the align_block API does).
-template <typename IdT, int NW, bool CG, bool PAD = true>
+// smem: NW*E + 2E + 1 + 32 ints.  pad = write the -1 padding of every expert run
+// (the weight-streaming kernels never read it; the align_block API and the
+// tcgen05 path's row packing do).
+template <typename IdT, int NW, bool CG>
 __device__ __forceinline__ void permute_block(const IdT* __restrict__ ids, const float* __restrict__ w,
-                                              int T, int K, int E, int bs, const PlanDev& p, int* smem) {
+                                              int T, int K, int E, int bs, const PlanDev& p, int* smem,
+                                              bool pad = true) {
   int* hist = smem;                 // [NW][E]
   int* off_s = hist + NW * E;       // [E + 1]
   int* scratch = off_s + E + 1;     // [32]
@@ -284,7 +286,7 @@ __device__ __forceinline__ void permute_block(const IdT* __restrict__ ids, const
     __syncwarp();
   }
 
-  if constexpr (PAD) {
+  if (pad) {
     for (int e = warp; e < E; e += NW) {
       const int real_end = off_s[e] + cnt_s[e];
       for (int q = real_end + lane; q < off_s[e + 1]; q += 32) {
