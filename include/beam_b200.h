@@ -165,9 +165,9 @@ int beam_profile_end(float* stage_ms, int* calls);
  * {first CTA start, last CTA start, first / last projection done,
  *  last top-K tile done, permute done, last top-K tile start, permute start}. */
 int beam_trace_gate(unsigned long long* dev_buf);
-/* Phase timeline of the fused decode kernel: u64[24], slot 2m = min and 2m+1 =
- * max over CTAs of %globaltimer at mark m (caller initialises even slots to ~0,
- * odd slots to 0); NULL disables. */
+/* Phase timeline of the fused decode kernel: u64[64 + 12 * grid] (zeroed by the
+ * caller); slot 64 + m * grid + cta = %globaltimer of CTA `cta` at mark m, slots
+ * 24..63 = CTA 0 sub-step clocks; NULL disables. */
 int beam_trace_decode(unsigned long long* dev_buf);
 const char* beam_last_cuda_error(void);
 const char* beam_build_info(void);

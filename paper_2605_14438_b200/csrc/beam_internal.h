@@ -1,6 +1,7 @@
 // Internal launcher declarations shared by the .cu translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -146,6 +147,7 @@ inline cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, con
 }
 
 // experts_tc.cu (tcgen05 grouped GEMM, prefill)
+bool make_tmap_rows_sw128(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 bool tc_supported(const beam_layer_t& L, const Dims& g);
 cudaError_t launch_pack_x(const void* h, int h_dtype, const float* inv, const float* nw, const Dims& g,
                           const PlanDev& p, int cap, void* xperm, cudaStream_t s);

@@ -721,6 +721,26 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t c
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+}  // namespace tc
+
+// 3-D view (64 columns, rows, cols / 64) of a row-major bf16 [rows, cols] matrix
+// with 128-byte swizzling: one box = box_rows rows x all columns, laid out in
+// shared memory as [cols / 64][box_rows][64] with the 16-byte chunks of every
+// 128-byte row XOR-permuted by (row index mod 8) — ldmatrix-conflict-free.
+bool make_tmap_rows_sw128(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  tc::EncodeTiledFn fn = tc::encode_fn();
+  if (!fn || cols % 64 != 0 || cols / 64 > 256 || box_rows > 256) return false;
+  const cuuint64_t dims[3] = {64, rows, cols / 64};
+  const cuuint64_t strides[2] = {cols * 2, 128};
+  const cuuint32_t box[3] = {64, box_rows, (cuuint32_t)(cols / 64)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace tc {
+
 static size_t smem_bytes(int E) {
   return 1024 + (size_t)kStages * (kABytes + kBBytes) + kStgBytes + (2 * kStages + 4) * 8 + 16 + (size_t)(E + 1) * 4;
 }

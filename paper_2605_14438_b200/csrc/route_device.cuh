@@ -75,18 +75,33 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
     av[i] = 0.0f;
     rank[i] = -1;
   }
+  // Loads are unconditional (clamped split / expert index, masked add) and issued
+  // four splits at a time: conditional loads inside the unrolled loop would be
+  // serialised, one L2 round trip each.  The sum runs in split order.
+  constexpr int kSB = MAXSPLIT < 4 ? MAXSPLIT : 4;
 #pragma unroll
-  for (int sp = 0; sp < MAXSPLIT; ++sp) {
-    if (sp < splits) {
-      const float* row = L + ((size_t)sp * T + t) * 2 * N;
+  for (int sp0 = 0; sp0 < MAXSPLIT; sp0 += kSB) {
+    if (sp0 < splits) {
+      float pv[kSB][NPL], pa[kSB][NPL];
 #pragma unroll
-      for (int i = 0; i < NPL; ++i) {
-        const int j = lane + 32 * i;
-        if (j < N) {
-          v[i] += ld_maybe_cg<CG>(row + j);
-          av[i] += ld_maybe_cg<CG>(row + N + j);
+      for (int q = 0; q < kSB; ++q) {
+        const float* row = L + ((size_t)min(sp0 + q, splits - 1) * T + t) * 2 * N;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) {
+          const int j = min(lane + 32 * i, N - 1);
+          pv[q][i] = ld_maybe_cg<CG>(row + j);
+          pa[q][i] = ld_maybe_cg<CG>(row + N + j);
         }
       }
+#pragma unroll
+      for (int q = 0; q < kSB; ++q)
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) {
+          if (sp0 + q < splits) {
+            v[i] += pv[q][i];
+            av[i] += pa[q][i];
+          }
+        }
     }
   }
 #pragma unroll

@@ -29,7 +29,8 @@ def main(tokens=(1, 8, 64), sparsities=(0.0, 0.5), flush_l2=True):
     blk = B.MoEBlock.from_weights(cfg, w["router"], (w["wg"], w["wu"], w["wd"]), norm_w=None,
                                   mask_w=w["mask"], dtype=torch.bfloat16, device=dev)
     lib = _lib.load()
-    tr = torch.zeros(24, dtype=torch.int64, device=dev)
+    G = torch.cuda.get_device_properties(0).multi_processor_count
+    tr = torch.zeros(64 + 12 * G, dtype=torch.int64, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     for t in tokens:
         for sp in sparsities:
@@ -38,12 +39,11 @@ def main(tokens=(1, 8, 64), sparsities=(0.0, 0.5), flush_l2=True):
             blk.mask_router.weight.copy_(bench.mask_with_theta(w["mask"], theta).to(dev))
             h = hc.to(dev)
             outs = LayerOutputs(t, Q["d"], Q["n"], Q["k"], h.dtype, dev)
-            rows = []
+            rows, clk = [], []
             for it in range(10):
                 if flush_l2:
                     flush.zero_()
                 tr.zero_()
-                tr[0::2] = np.iinfo(np.int64).max
                 torch.cuda.synchronize()
                 lib.beam_trace_decode(ctypes.c_void_p(tr.data_ptr()))
                 layer_forward_into(h, blk, outs)
@@ -51,12 +51,17 @@ def main(tokens=(1, 8, 64), sparsities=(0.0, 0.5), flush_l2=True):
                 lib.beam_trace_decode(None)
                 v = tr.cpu().numpy().astype(np.float64)
                 if it >= 2:
-                    t0 = v[0]
-                    rows.append([(v[2 * m] - t0, v[2 * m + 1] - t0) for m in NAMES])
+                    marks = v[64:].reshape(12, G)
+                    t0 = marks[0].min()
+                    rows.append([(marks[m].min() - t0, marks[m].max() - t0) if marks[m].max() > 0 else (0, 0)
+                                 for m in NAMES])
+                    clk.append(np.concatenate([v[38:40], v[24:28], v[28:31], v[32:34], v[44:45], v[40:44], v[36:38]]))
             med = np.median(np.array(rows), axis=0) / 1e3
             print(f"T={t} s={sp} flush={flush_l2}: " +
-                  ", ".join(f"{NAMES[m]}={lo:.1f}/{hi:.1f}" for m, (lo, hi) in zip(NAMES, med)), flush=True)
+                  ", ".join(f"{NAMES[m]}={lo:.1f}/{hi:.1f}" for m, (lo, hi) in zip(NAMES, med)) +
+                  " | clk proj stage/compute; topk load/rank/softmax/out; plan stage/scan/place; P4 sum wait/item, item=afrag/mma/release/sync/final; P5 sum wait/compute = " +
+                  "/".join(f"{x:.0f}" for x in np.median(np.array(clk), axis=0)), flush=True)
 
 
 if __name__ == "__main__":
-    main()
+    main(flush_l2=("--no-flush" not in sys.argv))
