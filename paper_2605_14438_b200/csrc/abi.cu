@@ -110,7 +110,7 @@ static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, La
   w.act16 = w.tc ? c.take<__nv_bfloat16>(cap * g.f_pad) : nullptr;
   w.xpad = g.d != g.d_pad ? c.take<float>((size_t)T * g.d_pad) : nullptr;
   w.inv = c.take<float>((size_t)T);
-  w.logits2 = c.take<float>((size_t)(T <= 64 ? 16 : 1) * T * 2 * g.N);  // split-K partials (<= 16 splits)
+  w.logits2 = c.take<float>((size_t)(T <= 64 ? 16 : 3) * T * 2 * g.N);  // split-K partials (<= 16 / 3 splits)
   w.ids32 = c.take<int32_t>(M);
   w.gw = c.take<float>(M);
   w.plan.counts = c.take<int32_t>(g.E);
@@ -226,12 +226,16 @@ static cudaError_t run_gate(const beam_layer_t& L, const Dims& g, const void* X,
                             const beam_outputs_t* o, LayerWs& w, cudaStream_t s) {
   const float* nw = L.has_norm ? L.norm_w : nullptr;
   cudaError_t e;
-  if (w.rscratch && router_tc_supported(T, 2 * g.N, g.d_pad, h_dtype))
+  int splits;
+  if (w.rscratch && router_tc_supported(T, 2 * g.N, g.d_pad, h_dtype)) {
     e = launch_router_tc(X, nw, L.gate_wT, T, 2 * g.N, g.d, g.d_pad, w.logits2, w.rscratch, s);
-  else
+    splits = router_tc_splits();
+  } else {
     e = launch_router(X, h_dtype, nw, L.gate_wT, T, 2 * g.N, g.d, g.d_pad, w.logits2, s);
+    splits = router_splits(T, 2 * g.N, g.d_pad);
+  }
   if (e != cudaSuccess) return e;
-  return launch_topk_mask(w.logits2, router_splits(T, 2 * g.N, g.d_pad), X, h_dtype, T, topk_args(L, g, o, w), s);
+  return launch_topk_mask(w.logits2, splits, X, h_dtype, T, topk_args(L, g, o, w), s);
 }
 
 int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, int T,

@@ -154,6 +154,7 @@ cudaError_t launch_pack_x(const void* h, int h_dtype, const float* inv, const fl
 void set_gemm_variant(int v);  // 0 = 2-SM pairs when possible, 1 = 1-SM kernel
 bool router_tc_supported(int T, int cols, int d_pad, int x_dtype);
 size_t router_tc_scratch_bytes(int cols, int d_pad);
+int router_tc_splits();  // split-K partials the tensor-core router writes
 cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* gate_wT, int T, int cols, int d,
                              int d_pad, float* P, void* scratch, cudaStream_t s);
 // opair written as bf16 [cap, d_pad] (combine reads it with BEAM_BF16)

@@ -38,7 +38,7 @@ __device__ __forceinline__ void ld_pair8(const TP* p, float* v) {
 }
 
 template <typename TH, typename TO, typename TP>
-__global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const int32_t* __restrict__ slot_expert,
+__global__ void __launch_bounds__(32 * kCombineWarps, 3) combine_kernel(const int32_t* __restrict__ slot_expert,
                                                                      const int32_t* __restrict__ slot_pos,
                                                                      const TP* __restrict__ opair, int T, int Keff,
                                                                      int d, int d_pad, const TH* __restrict__ h,
@@ -84,18 +84,34 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const int32
         unpack<float>(__ldg(hp + 1), hv + 4);
       }
     }
-    for (int r0 = 0; r0 < nv; r0 += 8) {
-      float v[8][8];
+    // rows stay packed in registers until their (ordered) add: 4 regs per bf16
+    // row, so 8 rows in flight cost 32 registers, not 64 (occupancy = bytes in
+    // flight for this HBM-bound gather)
+    constexpr int kRows = sizeof(TP) == 2 ? 8 : 4;
+    constexpr int kL = sizeof(TP) == 2 ? 1 : 2;
+    for (int r0 = 0; r0 < nv; r0 += kRows) {
+      uint4 raw[kRows][kL];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < kRows; ++q) {
         const int pr = __shfl_sync(0xffffffffu, sorted_pos, r0 + q < nv ? r0 + q : 0);
-        if (r0 + q < nv && c0 < d) ld_pair8<TP>(opair + (size_t)pr * d_pad + c0, v[q]);
+        if (r0 + q < nv && c0 < d) {
+          const uint4* src = reinterpret_cast<const uint4*>(opair + (size_t)pr * d_pad + c0);
+#pragma unroll
+          for (int l = 0; l < kL; ++l) raw[q][l] = __ldg(src + l);
+        }
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < kRows; ++q)
         if (r0 + q < nv) {
+          float v[8];
+          if constexpr (kL == 1) {
+            unpack<__nv_bfloat16>(raw[q][0], v);
+          } else {
+            unpack<float>(raw[q][0], v);
+            unpack<float>(raw[q][1], v + 4);
+          }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) y[i] += v[q][i];
+          for (int i = 0; i < 8; ++i) y[i] += v[i];
         }
     }
     if (vrow) {

@@ -58,6 +58,7 @@ struct Args {
   void* opair;  // mode 1: [cap, d_pad] bf16 per-pair rows; mode 2: fp32 logits
   int d_pad;
   int bn;  // token-tile width (<= BN, multiple of 16): narrower tiles spread few-expert GEMMs over more SMs
+  int p_cols, p_T;  // mode 2: logits P[split][p_T][p_cols], split = A row / p_cols
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -236,10 +237,13 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const Tile& tl, 
 #pragma unroll
       for (int j = 0; j < 32; ++j) s[j * BM + 32 * w4 + lane] = v[j];
       epi_bar(bar);
+      // A rows are [split][p_cols] (split-K over the bf16 terms of W): row block
+      // m_tile*BM lies inside one split
+      const int r0 = tl.m_tile * BM, sp = r0 / args.p_cols, col0 = r0 % args.p_cols;
+      float* P = reinterpret_cast<float*>(args.opair) + ((size_t)sp * args.p_T) * args.p_cols + col0;
       for (int row = w4; row < rows; row += 4) {
         const float4 val = reinterpret_cast<const float4*>(s + row * BM)[lane];
-        reinterpret_cast<float4*>(reinterpret_cast<float*>(args.opair) + (size_t)(tl.b_row0 + c0 + row) * args.m_rows +
-                                  tl.m_tile * BM)[lane] = val;
+        reinterpret_cast<float4*>(P + (size_t)(tl.b_row0 + c0 + row) * args.p_cols)[lane] = val;
       }
     }
     epi_bar(bar);  // staging reused by the next chunk
@@ -635,19 +639,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
 }
 
-// x_n rows in plan order, bf16 (B operand of GEMM1): X[p] = bf16(h[tok_p] * inv * w)
+// x_n rows in plan order, bf16 (B operand of GEMM1): X[p] = bf16(h[tok_p] * inv * w).
+// One warp per row, every 16-byte chunk of the row loaded before any is written
+// (raw registers: 4 per bf16 chunk); without a norm a bf16 row is a plain copy.
 template <typename TX>
 __global__ void __launch_bounds__(256) pack_x_kernel(const TX* __restrict__ h, const float* __restrict__ inv,
                                                      const float* __restrict__ nw, int d, int d_pad,
                                                      PlanDev p, int cap, __nv_bfloat16* __restrict__ X) {
   extern __shared__ float nws[];  // norm weights (zero-padded to d_pad), shared by all rows
-  for (int k = threadIdx.x; k < d_pad; k += blockDim.x) nws[k] = nw ? (k < d ? nw[k] : 0.0f) : 1.0f;
+  if (nw)
+    for (int k = threadIdx.x; k < d_pad; k += blockDim.x) nws[k] = k < d ? nw[k] : 0.0f;
   __syncthreads();
   griddep_wait();
-  const int total = p.meta[1];
+  const int total = min(p.meta[1], cap);
   const int lane = threadIdx.x & 31;
-  constexpr int kU = 8;  // 16-byte stripes per lane in flight
-  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < min(total, cap); row += gridDim.x * 8) {
+  constexpr int kL = sizeof(TX) == 2 ? 1 : 2;  // 16-byte loads per 8 elements
+  constexpr int kU = sizeof(TX) == 2 ? 8 : 4;  // 8-element chunks per lane in flight
+  const bool scale = inv != nullptr || nw != nullptr;
+  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < total; row += gridDim.x * 8) {
     const int tok = p.tok[row];
     __nv_bfloat16* dst = X + (size_t)row * d_pad;
     if (tok < 0) {
@@ -657,34 +666,37 @@ __global__ void __launch_bounds__(256) pack_x_kernel(const TX* __restrict__ h, c
     const float s = inv ? inv[tok] : 1.0f;
     const TX* src = h + (size_t)tok * d_pad;
     for (int k0 = lane * 8; k0 < d_pad; k0 += 256 * kU) {
-      float x[kU][8];
+      uint4 raw[kU][kL];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {  // all loads first
-        const int k = k0 + 256 * u;
-        if (k < d_pad) {
-          if constexpr (sizeof(TX) == 2) {
-            unpack<__nv_bfloat16>(ld_cached(src + k), x[u]);
-          } else {
-            unpack<float>(ld_cached(src + k), x[u]);
-            unpack<float>(ld_cached(src + k + 4), x[u] + 4);
-          }
-        }
+        const int k = min(k0 + 256 * u, d_pad - 8);
+#pragma unroll
+        for (int l = 0; l < kL; ++l) raw[u][l] = ld_cached(src + k + 4 * l);
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int k = k0 + 256 * u;
-        if (k < d_pad) {
-          uint32_t o[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            // x_n = (x * inv_rms) * w (tensor.py:487)
-            const float a = (x[u][2 * q] * s) * nws[k + 2 * q];
-            const float b = (x[u][2 * q + 1] * s) * nws[k + 2 * q + 1];
-            const __nv_bfloat162 v2 = __floats2bfloat162_rn(a, b);
-            o[q] = *reinterpret_cast<const uint32_t*>(&v2);
-          }
-          *reinterpret_cast<uint4*>(dst + k) = make_uint4(o[0], o[1], o[2], o[3]);
+        if (k >= d_pad) continue;
+        if (sizeof(TX) == 2 && !scale) {
+          *reinterpret_cast<uint4*>(dst + k) = raw[u][0];
+          continue;
         }
+        float x[8];
+        if constexpr (kL == 1) {
+          unpack<__nv_bfloat16>(raw[u][0], x);
+        } else {
+          unpack<float>(raw[u][0], x);
+          unpack<float>(raw[u][1], x + 4);
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          // x_n = (x * inv_rms) * w (tensor.py:487)
+          const float g0 = nw ? nws[k + 2 * q] : 1.0f, g1 = nw ? nws[k + 2 * q + 1] : 1.0f;
+          const __nv_bfloat162 v2 = __floats2bfloat162_rn((x[2 * q] * s) * g0, (x[2 * q + 1] * s) * g1);
+          o[q] = *reinterpret_cast<const uint32_t*>(&v2);
+        }
+        *reinterpret_cast<uint4*>(dst + k) = make_uint4(o[0], o[1], o[2], o[3]);
       }
     }
   }
@@ -862,10 +874,11 @@ cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* 
 // Prefill router / mask-router projection on the tensor cores.
 // logits = h . (w_norm o W)^T with h bf16 (exact) and W split into three bf16
 // terms W ~= hi + mid + lo (24 significant bits): the three products are exact
-// in fp32 and accumulate in fp32 in TMEM, i.e. fp32-accurate routing at
-// bf16 tensor-core speed.  The splits are laid side by side along K (A row c =
-// [hi | mid | lo]); B (= h) wraps every d_pad/64 k-blocks, so one GEMM of
-// K = 3 d_pad produces the sum.
+// in fp32 and accumulate in fp32, i.e. fp32-accurate routing at bf16
+// tensor-core speed.  The three terms are stacked as 3 row blocks of A (M =
+// 3 * cols): three split-K partial products [3][T][cols] that the top-K kernel
+// sums in order, and three times more work units than one K = 3 d_pad GEMM
+// (the tile count, not the FLOPs, bounds this small GEMM).
 // ---------------------------------------------------------------------------
 __global__ void split_router_kernel(const float* __restrict__ W, const float* __restrict__ nw, int cols, int d,
                                     int d_pad, __nv_bfloat16* __restrict__ A3, int T, int32_t* __restrict__ plan1) {
@@ -877,10 +890,10 @@ __global__ void split_router_kernel(const float* __restrict__ W, const float* __
     const float r1 = w - __bfloat162float(hi);
     const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
     const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-    __nv_bfloat16* row = A3 + (size_t)c * 3 * d_pad;
-    row[k] = hi;
-    row[d_pad + k] = mid;
-    row[2 * d_pad + k] = lo;
+    // [3][cols][d_pad]: the three terms are three row blocks (split-K units)
+    A3[(size_t)c * d_pad + k] = hi;
+    A3[((size_t)cols + c) * d_pad + k] = mid;
+    A3[((size_t)2 * cols + c) * d_pad + k] = lo;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     plan1[0] = T;  // counts[0]
@@ -894,6 +907,8 @@ bool router_tc_supported(int T, int cols, int d_pad, int x_dtype) {
 
 size_t router_tc_scratch_bytes(int cols, int d_pad) { return (size_t)cols * 3 * d_pad * 2 + 256; }
 
+int router_tc_splits() { return 3; }
+
 cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* gate_wT, int T, int cols, int d,
                              int d_pad, float* P, void* scratch, cudaStream_t s) {
   using namespace tc;
@@ -903,7 +918,7 @@ cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* ga
       gate_wT, norm_w, cols, d, d_pad, A3, T, plan1);
   count_launches(1);
   CUtensorMap mA, mB;
-  if (!make_map(&mA, A3, (uint64_t)cols, 3ull * d_pad, BM) || !make_map(&mB, X, (uint64_t)T, d_pad, kBBox))
+  if (!make_map(&mA, A3, 3ull * cols, d_pad, BM) || !make_map(&mB, X, (uint64_t)T, d_pad, kBBox))
     return cudaErrorInvalidValue;
   // one "expert" of T tokens: narrow the token tiles until the units cover the SMs
   static const int env_bn = [] {
@@ -911,7 +926,7 @@ cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* ga
     return v ? atoi(v) : 0;
   }();
   int bn = env_bn >= 16 && env_bn <= BN && env_bn % 16 == 0 ? env_bn : BN;
-  Args a{2, 1, cols, 3 * d_pad, d_pad / BK, plan1, plan1 + 1, nullptr, nullptr, 0, P, 0, bn};
+  Args a{2, 1, 3 * cols, d_pad, d_pad / BK, plan1, plan1 + 1, nullptr, nullptr, 0, P, 0, bn, cols, T};
   return launch_gemm(mA, mB, a, smem_bytes(1), true, s);
 }
 

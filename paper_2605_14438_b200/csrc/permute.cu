@@ -34,8 +34,8 @@ __global__ void __launch_bounds__(kPermuteThreads, 1)
 // ---------------------------------------------------------------------------
 constexpr int kMcThreads = 256;
 constexpr int kMcWarps = kMcThreads / 32;
-constexpr int kMcChunk = 4096;                  // entries per CTA
-constexpr int kMcPerWarp = kMcChunk / kMcWarps;  // 512, multiple of 32
+constexpr int kMcChunk = 1024;                  // entries per CTA (T*K / 1024 CTAs in flight)
+constexpr int kMcPerWarp = kMcChunk / kMcWarps;  // 128, multiple of 32
 constexpr long long kSingleCtaMax = 16384;
 
 // per-warp histograms of this CTA's chunk (shared), sh = [kMcWarps][E]
