@@ -59,6 +59,7 @@ struct Args {
   int d_pad;
   int bn;  // token-tile width (<= BN, multiple of 16): narrower tiles spread few-expert GEMMs over more SMs
   int p_cols, p_T;  // mode 2: logits P[split][p_T][p_cols], split = A row / p_cols
+  int apol;         // weight-tile L2 policy (a_policy)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -104,6 +105,17 @@ __device__ __forceinline__ uint64_t l2_policy(bool evict_first) {
   uint64_t p;
   if (evict_first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   else asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Weight (A) tile policy: evict-first when every weight tile is read by one unit
+// only (one token tile per expert), evict-normal when several token tiles of an
+// expert re-read it (prefill at low sparsity).  apol: 0 auto, 1 first, 2 normal, 3 last.
+__device__ __forceinline__ uint64_t a_policy(int apol, bool multi_ntile) {
+  uint64_t p;
+  if (apol == 3) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (apol == 2 || (apol == 0 && multi_ntile)) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 
@@ -353,11 +365,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      const uint64_t polA = l2_policy(args.mode != 2), polB = l2_policy(false);
+      const uint64_t polB = l2_policy(false);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = u0; t < total; t += ustep) {
         const Tile tl = decode(t, tile_off, E, MG, CM, rank, args);
+        const uint64_t polA = args.mode == 2 ? polB : a_policy(args.apol, tile_off[tl.e + 1] - tile_off[tl.e] > 1);
         const int nbox = (tl.nmma + kBBox - 1) / kBBox;
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -556,11 +569,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     if (lane == 0) {
-      const uint64_t polA = l2_policy(args.mode != 2), polB = l2_policy(false);
+      const uint64_t polB = l2_policy(false);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = u0; t < total; t += ustep) {
         const Tile tl = decode(t, tile_off, E, MG, 2, rank, args);
+        const uint64_t polA = args.mode == 2 ? polB : a_policy(args.apol, tile_off[tl.e + 1] - tile_off[tl.e] > 1);
         const int half = tl.nmma >> 1;  // token rows staged by each CTA
         const int nbox = (half + kBBox - 1) / kBBox;
         for (int kb = 0; kb < KB; ++kb) {
@@ -863,10 +877,14 @@ cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* 
       !make_map(&mB2, act16, (uint64_t)cap, g.f_pad, kBBox))
     return cudaErrorInvalidValue;
   const size_t smem = smem_bytes(g.E);
-  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN};
+  static const int apol = [] {
+    const char* v = getenv("BEAM_GEMM_APOL");  // tuning knob (a_policy)
+    return v ? atoi(v) : 0;
+  }();
+  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN, 0, 0, apol};
   cudaError_t e = launch_gemm(mA1, mB1, a1, smem, true, s);
   if (e != cudaSuccess) return e;
-  Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN};
+  Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN, 0, 0, apol};
   return launch_gemm(mA2, mB2, a2, smem, true, s);
 }
 
