@@ -161,12 +161,29 @@ class ClockSampler:
 
 
 def measured_peaks():
+    """(HBM GB/s, bf16 TFLOP/s burst, bf16 TFLOP/s sustained, kind)."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         with open(path) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), float(p.get("bf16_tflops", 1628.7)), "measured"
-    return 6650.0, 1590.0, "fallback"
+        burst = float(p.get("bf16_tflops", 1628.7))
+        return float(p["hbm_gbs"]), burst, float(p.get("bf16_tflops_sustained", burst)), "measured"
+    return 6650.0, 1590.0, 1590.0, "fallback"
+
+
+def ncu_traffic(kernel: str, workload: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary
+    (profiles/ncu_summary.json, written from an `ncu --set full` capture of the
+    same workload), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        rows = json.load(fh).get("kernels", [])
+    for r in rows:
+        if r.get("kernel") == kernel and r.get("workload") == workload:
+            return r.get("dram_bytes_per_launch")
+    return None
 
 
 def cpu_cores_used():
@@ -353,7 +370,7 @@ def run_ours(args):
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(dev)
     lib = _lib.load()
-    hbm_peak, tc_peak, peak_kind = measured_peaks()
+    hbm_peak, tc_peak, tc_peak_sus, peak_kind = measured_peaks()
     B.set_expert_path(args.expert_path)
     d, f, n, k = Q30["d"], Q30["f"], Q30["n"], Q30["k"]
     cfg = B.MoEBlockConfig(d_h=d, d_ff=f, num_experts=n, top_k=k)
@@ -369,8 +386,11 @@ def run_ours(args):
     launches0 = lib.beam_kernel_launches()
     with ClockSampler(dev.index) as clocks:
         pt = run_point(B, w, t, s, args.steps, args.warmup, flush, dev)
-    launches_per_step = 7
     ms = pt["ms"]
+    c0 = lib.beam_kernel_launches()
+    pt["layer"].eager()  # the graph replays exactly this launch sequence
+    torch.cuda.synchronize()
+    launches_per_step = int(lib.beam_kernel_launches() - c0)
     value = t / (ms / 1e3)
     layer = pt["layer"]
 
@@ -445,6 +465,7 @@ def run_ours(args):
                               "us_per_step": round(p["ms"] * 1e3, 1), "tokens_per_s": round(8192 / sec, 1),
                               "expert_tflops": round(flops / sec / 1e12, 2),
                               "tensor_frac_of_measured": round(flops / sec / 1e12 / tc_peak, 4),
+                              "tensor_frac_of_sustained": round(flops / sec / 1e12 / tc_peak_sus, 4),
                               "hbm_frac_of_measured": round(byt / sec / 1e9 / hbm_peak, 4)})
                 del p
 
@@ -464,7 +485,8 @@ def run_ours(args):
                 "path": "paper_2605_14438_b200.beam_block_forward(pinned host h) -> host outputs"},
         "roofline": {"bound": "hbm", "kernel": "gateup_kernel (experts gate/up, weight streaming)",
                      "achieved": gu_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gu_gbs / hbm_peak,
-                     "peak_kind": peak_kind, "traffic": None,
+                     "peak_kind": peak_kind + " (copy bandwidth, MEASURED_PEAKS.json hbm_gbs)",
+                     "traffic": ncu_traffic("gateup_warp_kernel" if t > 2 else "gateup_cta_kernel", f"T={t} s={s}"),
                      "algorithmic_bytes_per_launch": gu_bytes,
                      "layer": {"bytes": layer_bytes, "achieved_gbs": layer_bytes / (ms * 1e-3) / 1e9,
                                "frac": layer_bytes / (ms * 1e-3) / 1e9 / hbm_peak},
@@ -473,7 +495,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "parity_vs_reference_max_rel_err": parity,
         "clocks": clocks.summary(),
-        "gpu_launches": launches_per_step * (args.steps + args.warmup),
+        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches_per_step": launches_per_step,
         "gpu_launches_counted_total": int(launches),
         "sweep": sweep,
     }

@@ -23,6 +23,9 @@ namespace beam {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+// CTA-item kernels (T <= 2): resident CTAs per SM = weight bytes in flight per SM
+// (32 KB each); the warp-item kernels keep 2.
+constexpr int kCtaPerSm = 2;
 
 // EPC consecutive input elements (at a multiple of EPC) as floats.
 template <typename TX, int EPC>
@@ -110,7 +113,7 @@ __device__ __forceinline__ void gateup_cta_tile(const TW* __restrict__ W, int ro
 }
 
 template <typename TW, typename TX, int ACT>
-__global__ void __launch_bounds__(kThreads, 2) gateup_cta_kernel(const TW* __restrict__ Wgu,
+__global__ void __launch_bounds__(kThreads, kCtaPerSm) gateup_cta_kernel(const TW* __restrict__ Wgu,
                                                              const TX* __restrict__ X,
                                                              const float* __restrict__ inv,
                                                              const float* __restrict__ nw, int d,
@@ -128,13 +131,9 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_cta_kernel(const TW* __res
     const TW* W = Wgu + (size_t)e * 2 * f_pad * d_pad;
     const int feat0 = g * 4;
     const int row_g = (feat0 >> 4) * 32 + (feat0 & 15);
-    for (int t0 = 0; t0 < cnt;) {
+    for (int t0 = 0; t0 < cnt;) {  // T <= 2 (small_batch): at most 2 tokens per expert
       const int r = cnt - t0;
-      if (r >= 3) {
-        gateup_cta_tile<TW, TX, ACT, 4>(W, row_g, X, inv, nw, d, d_pad, f_pad, feat0, p.tok + off + t0,
-                                    off + t0, min(r, 4), act, part, red);
-        t0 += 4;
-      } else if (r == 2) {
+      if (r >= 2) {
         gateup_cta_tile<TW, TX, ACT, 2>(W, row_g, X, inv, nw, d, d_pad, f_pad, feat0, p.tok + off + t0,
                                     off + t0, 2, act, part, red);
         t0 += 2;
@@ -215,7 +214,7 @@ __device__ __forceinline__ void down_cta_tile(const TW* __restrict__ W, int row0
 }
 
 template <typename TW>
-__global__ void __launch_bounds__(kThreads, 2) down_cta_kernel(const TW* __restrict__ Wd,
+__global__ void __launch_bounds__(kThreads, kCtaPerSm) down_cta_kernel(const TW* __restrict__ Wd,
                                                            const float* __restrict__ act, int d_pad,
                                                            int f_pad, PlanDev p,
                                                            float* __restrict__ opair) {
@@ -230,13 +229,9 @@ __global__ void __launch_bounds__(kThreads, 2) down_cta_kernel(const TW* __restr
     const int cnt = p.counts[e], off = p.offsets[e];
     const TW* W = Wd + (size_t)e * d_pad * f_pad;
     const int row0 = g * 16, rows_valid = min(16, d_pad - row0);
-    for (int t0 = 0; t0 < cnt;) {
+    for (int t0 = 0; t0 < cnt;) {  // T <= 2 (small_batch): at most 2 tokens per expert
       const int r = cnt - t0;
-      if (r >= 3) {
-        down_cta_tile<TW, 4>(W, row0, rows_valid, act, f_pad, d_pad, off + t0, min(r, 4), p.w + off + t0,
-                         opair, part, red);
-        t0 += 4;
-      } else if (r == 2) {
+      if (r >= 2) {
         down_cta_tile<TW, 2>(W, row0, rows_valid, act, f_pad, d_pad, off + t0, 2, p.w + off + t0, opair,
                          part, red);
         t0 += 2;
@@ -456,9 +451,9 @@ static bool small_batch(int T) { return T <= 2; }
 cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
                                const float* inv, const float* nw, const PlanDev& p, float* act,
                                cudaStream_t s) {
-  const int grid = num_sms() * 2;
   const bool xb = x_dtype == BEAM_BF16;
   const bool cta = small_batch(T);
+  const int grid = num_sms() * (cta ? kCtaPerSm : 2);
   if (L.wdtype == BEAM_BF16) {
     if (xb) gateup_dispatch<__nv_bfloat16, __nv_bfloat16>(L, g, X, inv, nw, p, act, grid, cta, s);
     else gateup_dispatch<__nv_bfloat16, float>(L, g, X, inv, nw, p, act, grid, cta, s);
@@ -472,8 +467,8 @@ cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void*
 
 cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const PlanDev& p,
                              const float* act, float* opair, cudaStream_t s) {
-  const int grid = num_sms() * 2;
   const bool cta = small_batch(T);
+  const int grid = num_sms() * (cta ? kCtaPerSm : 2);
   if (L.wdtype == BEAM_BF16) {
     if (cta) launch_pdl(down_cta_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
     else launch_pdl(down_warp_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);

@@ -110,36 +110,43 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
     av[i] *= inv;
   }
 
-  float top_val = 0.0f;
-  for (int r = 0; r < K; ++r) {
-    bool have = false;
-    float bv = 0.0f;
-    int bj = 0x7fffffff;
+  // Selection on 64-bit keys (order-preserving float bits << 32 | ~expert id):
+  // one max per butterfly level, and the key order is exactly the reference's
+  // (value desc, ties -> lower id, moe.py:116-119); NaN logits rank last.
+  // K rounds of a 5-level butterfly, one 64-bit shuffle per level.
+  unsigned long long key[NPL];
 #pragma unroll
-    for (int i = 0; i < NPL; ++i) {
-      const int j = lane + 32 * i;
-      if (j < N && rank[i] < 0 && (!have || v[i] > bv)) {  // ascending j in a lane: ties keep the lower j
-        have = true;
-        bv = v[i];
-        bj = j;
-      }
-    }
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    const unsigned fb = __float_as_uint(v[i]);
+    const unsigned ord = v[i] != v[i] ? 0u : ((fb & 0x80000000u) ? ~fb : (fb | 0x80000000u));
+    key[i] = j < N ? (((unsigned long long)ord << 32) | (unsigned)(~j)) : 0ull;
+  }
+  int top_j = 0;
+  for (int r = 0; r < K; ++r) {
+    unsigned long long best = key[0];
+#pragma unroll
+    for (int i = 1; i < NPL; ++i) best = key[i] > best ? key[i] : best;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-      const bool ohave = __shfl_xor_sync(0xffffffffu, (int)have, o) != 0;
-      if (ohave && (!have || ov > bv || (ov == bv && oj < bj))) {
-        bv = ov;
-        bj = oj;
-        have = true;
-      }
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+      best = other > best ? other : best;
     }
-    if (r == 0) top_val = bv;
+    const int bj = (int)(~(unsigned)(best & 0xffffffffull));
+    if (r == 0) top_j = bj;
 #pragma unroll
     for (int i = 0; i < NPL; ++i)
-      if (lane + 32 * i == bj) rank[i] = r;
+      if (lane + 32 * i == bj) {
+        rank[i] = r;
+        key[i] = 0ull;
+      }
   }
+  // the top logit (softmax shift) from the lane that holds expert top_j
+  float mine = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i)
+    if (lane + 32 * i == top_j) mine = v[i];
+  const float top_val = __shfl_sync(0xffffffffu, mine, top_j & 31);
 
   // softmax over the K kept logits (tensor.py:440-451): exp(l - max) / sum
   float part = 0.0f;
