@@ -460,7 +460,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // signal the leader's full barrier; the leader's commits release both CTAs'
 // stages (multicast); both epilogues release the leader's accumulator barrier.
 // ---------------------------------------------------------------------------
-constexpr int kStages2 = 5;
+constexpr int kStages2 = 6;
+constexpr int kMaxE2 = 256;  // experts the 2-SM kernel's shared tile prefix holds (6 stages fill the rest)
 constexpr int kBHalfBytes = (BN / 2) * BK * 2;  // 16 KB: 128 token rows
 
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
@@ -827,6 +828,8 @@ static cudaError_t launch_gemm_cm(const CUtensorMap& mA, const CUtensorMap& mB, 
 
 static size_t smem_bytes_2sm(int E) {
   using namespace tc;
+  static_assert(1024 + kStages2 * (kABytes + kBHalfBytes) + 2 * kStgBytes + (2 * kStages2 + 4) * 8 + 16 + (kMaxE2 + 1) * 4 <= 227 * 1024,
+                "2-SM GEMM shared memory");
   return 1024 + (size_t)kStages2 * (kABytes + kBHalfBytes) + 2 * kStgBytes + (2 * kStages2 + 4) * 8 + 16 +
          (size_t)(E + 1) * 4;
 }
@@ -836,7 +839,7 @@ static cudaError_t launch_gemm_2sm(const CUtensorMap& mA, const CUtensorMap& mB,
   using namespace tc;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(grouped_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes_2sm(kMaxE));
+    cudaFuncSetAttribute(grouped_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes_2sm(kMaxE2));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -861,7 +864,7 @@ static cudaError_t launch_gemm(const CUtensorMap& mA, const CUtensorMap& mB, con
                                bool pdl, cudaStream_t s) {
   const int mt = a.m_rows / tc::BM;
   pdl = pdl && pdl_enabled();
-  if (g_gemm_variant == 0 && mt % 2 == 0) return launch_gemm_2sm(mA, mB, a, pdl, s);
+  if (g_gemm_variant == 0 && mt % 2 == 0 && a.E <= tc::kMaxE2) return launch_gemm_2sm(mA, mB, a, pdl, s);
   return launch_gemm_cm<1>(mA, mB, a, smem, pdl, s);
 }
 
