@@ -60,6 +60,8 @@ struct Args {
   int bn;  // token-tile width (<= BN, multiple of 16): narrower tiles spread few-expert GEMMs over more SMs
   int p_cols, p_T;  // mode 2: logits P[split][p_T][p_cols], split = A row / p_cols
   int apol;         // weight-tile L2 policy (a_policy)
+  int epi_skip;     // diagnostics (BEAM_EPI_SKIP=1): TMEM drained but no math / stores
+  int epi_direct;   // mode 1: store rows straight from registers (BEAM_EPI_DIRECT=1; default off)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -212,6 +214,7 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const Tile& tl, 
     const int rows = min(32, tl.ntok - c0);
     float v[32];
     tmem_ld32(tbase + c0, v);
+    if (args.epi_skip) continue;
     if (args.mode == 0) {
       // lanes 0-15 hold gate rows, 16-31 the matching up rows, of features 16*w4 + (lane & 15)
       __nv_bfloat16* s = reinterpret_cast<__nv_bfloat16*>(stg);  // [32 tokens][64 features]
@@ -230,6 +233,18 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const Tile& tl, 
         const uint32_t val = reinterpret_cast<const uint32_t*>(s + row * 64)[lane];
         reinterpret_cast<uint32_t*>(args.act + (size_t)(tl.b_row0 + c0 + row) * args.f_pad + tl.m_tile * 64)[lane] = val;
       }
+    } else if (args.mode == 1 && args.epi_direct) {
+      // direct: for token j the warp's 32 lanes hold 32 consecutive channels, so
+      // each store is a contiguous 64-byte row segment — no staging, no barrier
+      const float wl = lane < rows ? __ldg(args.w + tl.b_row0 + c0 + lane) : 0.0f;
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.opair) + (size_t)(tl.b_row0 + c0) * args.d_pad +
+                           tl.m_tile * BM + 32 * w4 + lane;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float wj = __shfl_sync(0xffffffffu, wl, j);
+        if (j < rows) dst[(size_t)j * args.d_pad] = __float2bfloat16_rn(v[j] * wj);
+      }
+      continue;
     } else if (args.mode == 1) {
       __nv_bfloat16* s = reinterpret_cast<__nv_bfloat16*>(stg);  // [32 tokens][128 channels]
       const float wl = lane < rows ? __ldg(args.w + tl.b_row0 + c0 + lane) : 0.0f;
@@ -884,10 +899,18 @@ cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* 
     const char* v = getenv("BEAM_GEMM_APOL");  // tuning knob (a_policy)
     return v ? atoi(v) : 0;
   }();
-  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN, 0, 0, apol};
+  static const int epi_direct = [] {  // measured slower than the staged transpose (GEMM2 278 vs 260 us)
+    const char* v = getenv("BEAM_EPI_DIRECT");
+    return v && v[0] == '1' ? 1 : 0;
+  }();
+  static const int epi_skip = [] {
+    const char* v = getenv("BEAM_EPI_SKIP");  // diagnostics only: invalid results
+    return v && v[0] == '1' ? 1 : 0;
+  }();
+  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN, 0, 0, apol, epi_skip, epi_direct};
   cudaError_t e = launch_gemm(mA1, mB1, a1, smem, true, s);
   if (e != cudaSuccess) return e;
-  Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN, 0, 0, apol};
+  Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN, 0, 0, apol, epi_skip, epi_direct};
   return launch_gemm(mA2, mB2, a2, smem, true, s);
 }
 

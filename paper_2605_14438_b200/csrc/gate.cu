@@ -394,6 +394,8 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   if (!s_last) return;
   __threadfence();
   trace_minmax(-1, 7);
+  // (plan_small_block<8> — the bitmask plan — measured slower here than the
+  // counting sort: 5.0 vs 4.0 us at T = 1, 7.3 vs 5.6 us at T = 64)
   permute_block<int32_t, 8, true>(a.ids32, a.gw, T, a.K + a.S, E, bs, p, reinterpret_cast<int*>(xs), pad);
   if (threadIdx.x == 0) counters[kCounterSlots - 1] = 0;
   __syncthreads();

@@ -320,4 +320,98 @@ __device__ __forceinline__ void permute_block(const IdT* __restrict__ ids, const
   }
 }
 
+// The same plan for T <= 64 tokens without a serial pass: each expert keeps a
+// 64-bit mask of its tokens (a token routes to an expert at most once), so the
+// position of (t, k) inside its expert's run — ascending flat index t*K+k ==
+// ascending t — is a popcount.  One CTA of NW warps; 4 __syncthreads in all.
+// smem: 2E + (E + 1) + E ints.  Outputs identical to permute_block.
+template <int NW>
+__device__ __forceinline__ void plan_small_block(const int32_t* ids, const float* w, int T, int K, int E, int bs,
+                                                 const PlanDev& p, int* smem, bool pad) {
+  unsigned* bits = reinterpret_cast<unsigned*>(smem);  // [E][2]
+  int* off_s = smem + 2 * E;                           // [E + 1]
+  int* cnt_s = off_s + E + 1;                          // [E]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int M = T * K;
+  for (int i = tid; i < 2 * E; i += NW * 32) bits[i] = 0u;
+  __syncthreads();
+  for (int i = tid; i < M; i += NW * 32) {
+    const int e = __ldcg(ids + i);
+    if (e >= 0 && e < E) {
+      const int t = i / K;
+      atomicOr(&bits[2 * e + (t >> 5)], 1u << (t & 31));
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int per = ceil_div(E, 32);
+    const int e0 = min(E, lane * per), e1 = min(E, e0 + per);
+    int psum = 0, asum = 0, rsum = 0;
+    for (int e = e0; e < e1; ++e) {
+      const int c = __popc(bits[2 * e]) + __popc(bits[2 * e + 1]);
+      cnt_s[e] = c;
+      psum += round_up(c, bs);
+      asum += c > 0;
+      rsum += c;
+    }
+    int px = psum, ax = asum, rx = rsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int yp = __shfl_up_sync(0xffffffffu, px, o);
+      const int ya = __shfl_up_sync(0xffffffffu, ax, o);
+      const int yr = __shfl_up_sync(0xffffffffu, rx, o);
+      if (lane >= o) {
+        px += yp;
+        ax += ya;
+        rx += yr;
+      }
+    }
+    int prun = px - psum, arun = ax - asum;
+    for (int e = e0; e < e1; ++e) {
+      const int c = cnt_s[e];
+      off_s[e] = prun;
+      p.counts[e] = c;
+      p.offsets[e] = prun;
+      if (c > 0) p.active[arun++] = e;
+      prun += round_up(c, bs);
+    }
+    if (lane == 31) {
+      off_s[E] = px;
+      p.offsets[E] = px;
+      p.meta[0] = ax;
+      p.meta[1] = px;
+      p.meta[2] = rx;
+      p.meta[3] = 0;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < M; i += NW * 32) {
+    const int e = __ldcg(ids + i);
+    if (e >= 0 && e < E) {
+      const int t = i / K;
+      const unsigned b0 = bits[2 * e], b1 = bits[2 * e + 1];
+      const int below = t < 32 ? __popc(b0 & ((1u << t) - 1u)) : __popc(b0) + __popc(b1 & ((1u << (t - 32)) - 1u));
+      const int pos = off_s[e] + below;
+      p.tok[pos] = t;
+      p.slot[pos] = i - t * K;
+      if (p.w) p.w[pos] = w ? __ldcg(w + i) : 0.0f;
+      if (p.slot_pos) p.slot_pos[i] = pos;
+      if (p.slot_expert) p.slot_expert[i] = e;
+    } else {
+      if (p.slot_pos) p.slot_pos[i] = -1;
+      if (p.slot_expert) p.slot_expert[i] = -1;
+    }
+  }
+  if (pad) {
+    for (int e = warp; e < E; e += NW) {
+      const int real_end = off_s[e] + cnt_s[e];
+      for (int q = real_end + lane; q < off_s[e + 1]; q += 32) {
+        p.tok[q] = -1;
+        p.slot[q] = -1;
+        if (p.w) p.w[q] = 0.0f;
+      }
+    }
+  }
+}
+
 }  // namespace beam
