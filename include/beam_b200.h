@@ -58,6 +58,29 @@ enum {
 enum { BEAM_F32 = 0, BEAM_BF16 = 1, BEAM_F64 = 2 };
 enum { BEAM_ACT_SILU = 0, BEAM_ACT_IDENTITY = 1 };
 
+/* Routing rules of baselines.route (baselines.py:158-283, inference branch). */
+enum {
+  BEAM_ROUTE_BEAM = 0,    /* binary expert-activation mask (beam)                       */
+  BEAM_ROUTE_TOPK = 1,    /* vanilla_topk / topk_reduced (k_small) / topk_pruning (k_infer) */
+  BEAM_ROUTE_DYNAMIC = 2, /* moe_dynamic: top-p prefix of the full softmax, mass >= phi     */
+  BEAM_ROUTE_ADA = 3,     /* ada_moe: top-K over N + null_count columns, nulls skipped      */
+  BEAM_ROUTE_SOFT = 4     /* soft_mask / soft_mask_tempered: sigmoid(a / temp) weights      */
+};
+
+/* One routing rule.  gate_wT of the layer holds, per kind: BEAM / SOFT
+ * [router N ; mask N] rows, TOPK / DYNAMIC [router N] (mask rows ignored),
+ * ADA [router N + null_count] (no mask). */
+typedef struct {
+  int kind;        /* BEAM_ROUTE_*                                                   */
+  int k;           /* candidates per token (k_eff for TOPK; top_k otherwise)         */
+  int null_count;  /* ADA: extra router columns                                      */
+  float phi;       /* DYNAMIC: probability mass                                     */
+  float temp;      /* SOFT: temperature (temp_floor for soft_mask_tempered, else 1) */
+  float tau;       /* SOFT: mask threshold probability                              */
+  int binarize;    /* SOFT: 1 -> weights * (sigmoid(a/temp) >= tau), masked slots skipped;
+                      0 -> weights * sigmoid(a/temp), every candidate executes      */
+} beam_route_t;
+
 /* Packed parameters of one BEAM MoE block (moe.py:169-192, beam.py:33-48).
  * Shapes use E = num_experts + num_shared, d_pad = round_up(d_h, 8),
  * f_pad = round_up(d_ff, 16).  Padding entries are zero.
@@ -101,6 +124,18 @@ size_t beam_workspace_bytes(const beam_layer_t* layer, int T, int K, int block_s
 int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, int T,
                        int block_size, const beam_outputs_t* outputs, void* workspace,
                        size_t workspace_bytes, beam_stream_t stream);
+
+/* baselines.block_forward(h, block, strategy, training=False, block_size)
+ * (baselines.py:286-323): the routing rule `route` (NULL = BEAM with the layer's
+ * mask_threshold), then the same masked permute / grouped experts / combine.
+ * Outputs: out; topk_ids [T, k] = RouteResult.candidate_ids; masked_ids [T, k] =
+ * kept_ids; logits [T, N (+ null_count)]; weights [T, N] = weights_hat; for BEAM /
+ * SOFT pre_activation, raw_mask (sigmoid(a / temp)) and mask (the hard bits). */
+int beam_layer_forward_routed(const beam_layer_t* layer, const beam_route_t* route, const void* h,
+                              int h_dtype, int T, int block_size, const beam_outputs_t* outputs,
+                              void* workspace, size_t workspace_bytes, beam_stream_t stream);
+size_t beam_workspace_bytes_routed(const beam_layer_t* layer, const beam_route_t* route, int T,
+                                   int block_size);
 
 /* The gating half alone (rms_norm -> topk_route -> mask_forward -> mask_route):
  * fills the decision outputs of `outputs` (outputs->out is ignored). */

@@ -324,3 +324,111 @@ def beam_block_forward(h: np.ndarray, block: OracleBlock, block_size: int = 16) 
     for e in block.shared:  # beam.py:163-164
         y = y + expert_forward(x_n, *e, block.activation)
     return LayerResult(h + y, decision, maskdec, masked_ids, plan, y)
+
+
+# ---------------------------------------------------------------------------
+# routing strategies (baselines.py) — inference branch
+# ---------------------------------------------------------------------------
+
+STRATEGY_KINDS = ("vanilla_topk", "topk_reduced", "topk_pruning", "moe_dynamic", "ada_moe",
+                  "beam", "soft_mask", "soft_mask_tempered")
+
+
+def softmax(x: np.ndarray) -> np.ndarray:
+    """tensor.py softmax over the last axis (max-shifted)."""
+    z = x - x.max(axis=-1, keepdims=True)
+    e = np.exp(z)
+    return e / e.sum(axis=-1, keepdims=True)
+
+
+def dynamic_select(probs: np.ndarray, phi: float) -> np.ndarray:
+    """baselines.py:132-143 — smallest descending-probability prefix whose
+    cumulative mass reaches phi, at least one expert per token."""
+    order = np.argsort(-probs, axis=-1, kind="stable")
+    csum = np.take_along_axis(probs, order, axis=-1).cumsum(axis=-1)
+    counts = np.minimum((csum < phi).sum(axis=-1) + 1, probs.shape[-1])
+    active = np.zeros(probs.shape, dtype=bool)
+    ranks = np.arange(probs.shape[-1])[None, :]
+    np.put_along_axis(active, order, ranks < counts[:, None], axis=-1)
+    return active
+
+
+@dataclass
+class RouteResult:
+    """baselines.py:116-129 (the fields the inference path produces)."""
+
+    weights_hat: np.ndarray
+    logits: np.ndarray
+    candidate_ids: np.ndarray
+    active_bits: np.ndarray
+    active_counts: np.ndarray
+    kept_ids: np.ndarray
+    raw_mask: np.ndarray | None = None
+
+
+def route(block: OracleBlock, x_n: np.ndarray, kind: str, params: dict | None = None,
+          binarize_soft: bool = False) -> RouteResult:
+    """baselines.py:158-283 with training=False.  ``block.router_w`` may carry
+    null columns (ada_moe, baselines.py:212-225)."""
+    p = params or {}
+    k = block.top_k
+    n = block.num_experts
+    if kind in ("vanilla_topk", "topk_reduced", "topk_pruning"):  # :173-190
+        k_eff = p.get("k_small", k) if kind == "topk_reduced" else (p.get("k_infer", k) if kind == "topk_pruning" else k)
+        dec = topk_route(x_n, block.router_w, k_eff)
+        ids = dec.topk_indices
+        return RouteResult(dec.weights, dec.logits, ids, np.ones(ids.shape, np.int64),
+                           np.full(ids.shape[0], k_eff, np.int64), ids)
+    if kind == "moe_dynamic":  # :192-210
+        logits = x_n @ block.router_w
+        probs = softmax(logits)
+        active = dynamic_select(probs, p.get("phi", 0.5))
+        masked = probs * active.astype(np.float64)
+        weights_hat = masked / masked.sum(axis=-1, keepdims=True)
+        order = topk_select(probs, k)
+        bits = np.take_along_axis(active, order, axis=-1).astype(np.int64)
+        counts = active.sum(axis=-1).astype(np.int64)
+        kept = np.where(bits == 1, order, np.int64(-1))
+        return RouteResult(weights_hat, logits, order, bits, counts, kept)
+    if kind == "ada_moe":  # :212-225
+        dec = topk_route(x_n, block.router_w, k)
+        ids_ext = dec.topk_indices
+        real = ids_ext < n
+        cand = np.where(real, ids_ext, np.int64(-1))
+        return RouteResult(dec.weights[:, :n], dec.logits, cand, real.astype(np.int64),
+                           real.sum(axis=-1).astype(np.int64), cand)
+    dec = topk_route(x_n, block.router_w, k)
+    ids = dec.topk_indices
+    tau = block.tau
+    if kind == "beam":  # :230-247
+        md = mask_forward(x_n, block.mask_w, tau)
+        bits = np.take_along_axis(md.mask.astype(np.int64), ids, axis=-1)
+        return RouteResult(dec.weights * md.mask, dec.logits, ids, bits, bits.sum(axis=-1),
+                           np.where(bits == 1, ids, np.int64(-1)), md.raw_mask)
+    # soft variants :250-283
+    temp = p.get("temp_floor", 0.1) if kind == "soft_mask_tempered" else 1.0
+    a = x_n @ block.mask_w
+    soft = sigmoid(a * (1.0 / temp))
+    hard = (soft >= tau).astype(np.int64)
+    bits_hard = np.take_along_axis(hard, ids, axis=-1)
+    if kind == "soft_mask_tempered" or binarize_soft:
+        weights_hat = dec.weights * (soft >= tau).astype(np.float64)
+        bits = bits_hard
+        kept = np.where(bits == 1, ids, np.int64(-1))
+    else:
+        weights_hat = dec.weights * soft
+        bits = np.ones(ids.shape, np.int64)
+        kept = ids
+    return RouteResult(weights_hat, dec.logits, ids, bits, bits.sum(axis=-1), kept, soft)
+
+
+def strategy_block_forward(h: np.ndarray, block: OracleBlock, kind: str, params: dict | None = None,
+                           binarize_soft: bool = False, block_size: int = 16):
+    """baselines.py:286-323, training=False -> (h + y, RouteResult)."""
+    x_n = block.normalize(h)
+    rr = route(block, x_n, kind, params, binarize_soft)
+    plan = align_block(rr.kept_ids, block_size, num_experts=block.num_experts)
+    y = grouped_execute(x_n, plan, block.experts, rr.weights_hat, block.activation)
+    for e in block.shared:
+        y = y + expert_forward(x_n, *e, block.activation)
+    return h + y, rr

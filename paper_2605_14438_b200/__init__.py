@@ -7,7 +7,7 @@ C ABI in ``include/beam_b200.h``.  No CPU fallback: without the built library
 or a CUDA device every compute entry raises ``BeamNativeError``.
 """
 
-from . import dispatch  # noqa: F401
+from . import baselines, dispatch  # noqa: F401
 from ._lib import BeamNativeError  # noqa: F401
 from .beam import MaskDecision, MaskRouter, beam_block_forward, mask_forward, rms_norm, set_expert_path  # noqa: F401
 from .moe import (  # noqa: F401
@@ -23,5 +23,5 @@ from .tensor import ContractError, NumericError, ShapeError  # noqa: F401
 __all__ = [
     "BeamNativeError", "ContractError", "Expert", "MaskDecision", "MaskRouter", "MoEBlock",
     "MoEBlockConfig", "NumericError", "RouterDecision", "ShapeError", "beam_block_forward",
-    "dispatch", "mask_forward", "rms_norm", "topk_route", "topk_select",
+    "baselines", "dispatch", "mask_forward", "rms_norm", "topk_route", "topk_select",
 ]

@@ -22,11 +22,14 @@ BEAM_ERR_WORKSPACE = -4
 
 BEAM_F32, BEAM_BF16, BEAM_F64 = 0, 1, 2
 BEAM_ACT_SILU, BEAM_ACT_IDENTITY = 0, 1
+BEAM_ROUTE_BEAM, BEAM_ROUTE_TOPK, BEAM_ROUTE_DYNAMIC, BEAM_ROUTE_ADA, BEAM_ROUTE_SOFT = 0, 1, 2, 3, 4
 
 # every symbol include/beam_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "beam_workspace_bytes",
     "beam_layer_forward",
+    "beam_layer_forward_routed",
+    "beam_workspace_bytes_routed",
     "beam_gate",
     "beam_moe_execute",
     "beam_mask_route",
@@ -68,6 +71,20 @@ class LayerDesc(ctypes.Structure):
     ]
 
 
+class RouteDesc(ctypes.Structure):
+    """beam_route_t."""
+
+    _fields_ = [
+        ("kind", ctypes.c_int),
+        ("k", ctypes.c_int),
+        ("null_count", ctypes.c_int),
+        ("phi", ctypes.c_float),
+        ("temp", ctypes.c_float),
+        ("tau", ctypes.c_float),
+        ("binarize", ctypes.c_int),
+    ]
+
+
 class Outputs(ctypes.Structure):
     """beam_outputs_t."""
 
@@ -96,10 +113,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             f"CUDA library not built: {path} missing (run `python -m paper_2605_14438_b200._build`)")
     lib = ctypes.CDLL(path)
     P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
-    LP, OP = ctypes.POINTER(LayerDesc), ctypes.POINTER(Outputs)
+    LP, OP, RP = ctypes.POINTER(LayerDesc), ctypes.POINTER(Outputs), ctypes.POINTER(RouteDesc)
     sig = {
         "beam_workspace_bytes": (S, [LP, I, I, I]),
         "beam_layer_forward": (I, [LP, P, I, I, I, OP, P, S, P]),
+        "beam_layer_forward_routed": (I, [LP, RP, P, I, I, I, OP, P, S, P]),
+        "beam_workspace_bytes_routed": (S, [LP, RP, I, I]),
         "beam_gate": (I, [LP, P, I, I, OP, P, S, P]),
         "beam_moe_execute": (I, [LP, P, I, I, I, P, P, P, P, S, P]),
         "beam_mask_route": (I, [P, P, I, I, I, I, P, P]),

@@ -94,8 +94,9 @@ struct LayerWs {
 
 // One layout serves every entry (sized for the largest user, beam_layer_forward).
 // x_bytes: element size of the activation rows (4 covers both dtypes).
-static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, LayerWs* o) {
+static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, LayerWs* o, int cols = 0) {
   const Dims g = dims_of(L);
+  if (cols < 2 * g.N) cols = 2 * g.N;  // projection columns (router [+ null] [+ mask])
   const int Krow = Kids > g.Keff ? Kids : g.Keff;
   const size_t M = (size_t)T * Krow;
   const size_t cap = M + (size_t)g.E * (size_t)(bs > 0 ? bs - 1 : 0);
@@ -103,14 +104,14 @@ static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, La
   LayerWs w;
   w.counters = c.take<int>(64);
   w.pscratch = c.take<int>(permute_scratch_bytes(T, Krow, g.E) / sizeof(int));
-  w.rscratch = T > 64 ? c.take<char>(router_tc_scratch_bytes(2 * g.N, g.d_pad)) : nullptr;
+  w.rscratch = T > 64 ? c.take<char>(router_tc_scratch_bytes(cols, g.d_pad)) : nullptr;
   w.tc = use_tc(L, g, T, Krow);
   w.cap = (int)cap;
   w.xperm = w.tc ? c.take<__nv_bfloat16>(cap * g.d_pad) : nullptr;
   w.act16 = w.tc ? c.take<__nv_bfloat16>(cap * g.f_pad) : nullptr;
   w.xpad = g.d != g.d_pad ? c.take<float>((size_t)T * g.d_pad) : nullptr;
   w.inv = c.take<float>((size_t)T);
-  w.logits2 = c.take<float>((size_t)(T <= 64 ? 16 : 3) * T * 2 * g.N);  // split-K partials (<= 16 / 3 splits)
+  w.logits2 = c.take<float>((size_t)(T <= 64 ? 16 : 3) * T * cols);  // split-K partials (<= 16 / 3 splits)
   w.ids32 = c.take<int32_t>(M);
   w.gw = c.take<float>(M);
   w.plan.counts = c.take<int32_t>(g.E);
@@ -199,12 +200,76 @@ size_t beam_workspace_bytes(const beam_layer_t* layer, int T, int K, int block_s
   return carve(*layer, T, K, block_size < 1 ? 1 : block_size, nullptr, nullptr);
 }
 
-static TopkArgs topk_args(const beam_layer_t& L, const Dims& g, const beam_outputs_t* o, LayerWs& w) {
+// A routing rule resolved against the layer (beam_route_t, NULL = BEAM).
+struct Spec {
+  int kind = BEAM_ROUTE_BEAM;
+  int K = 0, Keff = 0;        // candidates per token, + shared experts
+  int Nr = 0, cols = 0, mask_off = 0;
+  float phi = 0.5f, temp_inv = 1.0f, tau = 0.5f, thr = 0.0f;
+  int binarize = 1;
+};
+
+static int spec_of(const beam_layer_t& L, const beam_route_t* r, Spec* sp) {
+  const Dims g = dims_of(L);
+  Spec s;
+  s.thr = L.mask_threshold;
+  s.K = g.K;
+  s.Nr = g.N;
+  s.cols = 2 * g.N;
+  s.mask_off = g.N;
+  if (r != nullptr) {
+    s.kind = r->kind;
+    switch (r->kind) {
+      case BEAM_ROUTE_BEAM:
+        break;
+      case BEAM_ROUTE_TOPK:
+      case BEAM_ROUTE_DYNAMIC:
+        s.K = r->k;
+        s.cols = g.N;
+        s.mask_off = -1;
+        if (r->kind == BEAM_ROUTE_DYNAMIC && !(r->phi > 0.0f && r->phi <= 1.0f)) return BEAM_ERR_ARG;
+        s.phi = r->phi;
+        break;
+      case BEAM_ROUTE_ADA:
+        if (r->null_count < 0) return BEAM_ERR_ARG;
+        s.K = r->k;
+        s.Nr = g.N + r->null_count;
+        s.cols = s.Nr;
+        s.mask_off = -1;
+        break;
+      case BEAM_ROUTE_SOFT:
+        if (!(r->temp > 0.0f) || !(r->tau > 0.0f && r->tau < 1.0f)) return BEAM_ERR_ARG;
+        s.K = r->k;
+        s.temp_inv = 1.0f / r->temp;
+        s.tau = r->tau;
+        s.binarize = r->binarize != 0;
+        break;
+      default:
+        return BEAM_ERR_ARG;
+    }
+  }
+  if (s.K < 1 || s.K > s.Nr || s.Nr > 512) return BEAM_ERR_ARG;
+  if (s.K + g.S > 32) return BEAM_ERR_UNSUPPORTED;
+  s.Keff = s.K + g.S;
+  *sp = s;
+  return BEAM_OK;
+}
+
+static TopkArgs topk_args(const beam_layer_t& L, const Dims& g, const beam_outputs_t* o, LayerWs& w,
+                          const Spec& sp) {
   TopkArgs a;
   a.N = g.N;
-  a.K = g.K;
+  a.K = sp.K;
   a.S = g.S;
-  a.thr = L.mask_threshold;
+  a.thr = sp.thr;
+  a.kind = sp.kind;
+  a.Nr = sp.Nr;
+  a.cols = sp.cols;
+  a.mask_off = sp.mask_off;
+  a.phi = sp.phi;
+  a.temp_inv = sp.temp_inv;
+  a.tau = sp.tau;
+  a.binarize = sp.binarize;
   a.has_norm = L.has_norm;
   a.d = g.d;
   a.d_pad = g.d_pad;
@@ -223,42 +288,44 @@ static TopkArgs topk_args(const beam_layer_t& L, const Dims& g, const beam_outpu
 
 // The gating half shared by beam_layer_forward and beam_gate.
 static cudaError_t run_gate(const beam_layer_t& L, const Dims& g, const void* X, int h_dtype, int T,
-                            const beam_outputs_t* o, LayerWs& w, cudaStream_t s) {
+                            const beam_outputs_t* o, LayerWs& w, cudaStream_t s, const Spec& sp) {
   const float* nw = L.has_norm ? L.norm_w : nullptr;
   cudaError_t e;
   int splits;
-  if (w.rscratch && router_tc_supported(T, 2 * g.N, g.d_pad, h_dtype)) {
-    e = launch_router_tc(X, nw, L.gate_wT, T, 2 * g.N, g.d, g.d_pad, w.logits2, w.rscratch, s);
+  if (w.rscratch && router_tc_supported(T, sp.cols, g.d_pad, h_dtype)) {
+    e = launch_router_tc(X, nw, L.gate_wT, T, sp.cols, g.d, g.d_pad, w.logits2, w.rscratch, s);
     splits = router_tc_splits();
   } else {
-    e = launch_router(X, h_dtype, nw, L.gate_wT, T, 2 * g.N, g.d, g.d_pad, w.logits2, s);
-    splits = router_splits(T, 2 * g.N, g.d_pad);
+    e = launch_router(X, h_dtype, nw, L.gate_wT, T, sp.cols, g.d, g.d_pad, w.logits2, s);
+    splits = router_splits(T, sp.cols, g.d_pad);
   }
   if (e != cudaSuccess) return e;
-  return launch_topk_mask(w.logits2, splits, X, h_dtype, T, topk_args(L, g, o, w), s);
+  return launch_topk_mask(w.logits2, splits, X, h_dtype, T, topk_args(L, g, o, w, sp), s);
 }
 
-int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, int T,
-                       int block_size, const beam_outputs_t* o, void* workspace,
-                       size_t workspace_bytes, beam_stream_t stream) {
+static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, const void* h, int h_dtype, int T,
+                         int block_size, const beam_outputs_t* o, void* workspace, size_t workspace_bytes,
+                         beam_stream_t stream) {
   int rc = validate(layer);
   if (rc) return rc;
+  Spec sp;
+  if ((rc = spec_of(*layer, route, &sp)) != BEAM_OK) return rc;
   if (T < 0 || block_size < 1 || !o || !o->out || (T > 0 && !h)) return BEAM_ERR_ARG;
   if (h_dtype != BEAM_F32 && h_dtype != BEAM_BF16) return BEAM_ERR_ARG;
   if (T == 0) return BEAM_OK;
   const beam_layer_t& L = *layer;
   const Dims g = dims_of(L);
   LayerWs w;
-  if (carve(L, T, 0, block_size, workspace, &w) > workspace_bytes || !workspace)
+  if (carve(L, T, sp.Keff, block_size, workspace, &w, sp.cols) > workspace_bytes || !workspace)
     return BEAM_ERR_WORKSPACE;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const void* X = nullptr;
 
   prof_mark(0, s);
   BEAM_TRY(strided_input(g, h, h_dtype, T, w, &X, s));
-  if (!w.tc && g_expert_path.load() != 4 && decode_fused_supported(L, g, T)) {
+  if (sp.kind == BEAM_ROUTE_BEAM && !w.tc && g_expert_path.load() != 4 && decode_fused_supported(L, g, T)) {
     // decode: the whole layer in one persistent kernel
-    BEAM_TRY(launch_decode_fused(L, g, X, h_dtype, T, topk_args(L, g, o, w), w.logits2, w.act,
+    BEAM_TRY(launch_decode_fused(L, g, X, h_dtype, T, topk_args(L, g, o, w, sp), w.logits2, w.act,
                                  reinterpret_cast<unsigned*>(w.counters + 32), o->out, s));
     for (int m = 1; m < kStageMarks; ++m) prof_mark(m, s);
     return BEAM_OK;
@@ -266,12 +333,12 @@ int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, in
   if (gate_fused_supported(T, g.N, g.E, g.d_pad)) {
     // decode: projection + top-K + permute in one launch
     BEAM_TRY(launch_gate_fused(X, h_dtype, L.has_norm ? L.norm_w : nullptr, L.gate_wT, T, g.d, g.d_pad,
-                               w.logits2, topk_args(L, g, o, w), g.E, block_size, w.tc, w.plan, w.counters, s));
+                               w.logits2, topk_args(L, g, o, w, sp), g.E, block_size, w.tc, w.plan, w.counters, s));
     prof_mark(1, s);
   } else {
-    BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s));
+    BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s, sp));
     prof_mark(1, s);
-    BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, T, g.Keff, g.E, block_size, w.plan, w.pscratch, s));
+    BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, T, sp.Keff, g.E, block_size, w.plan, w.pscratch, s));
   }
   prof_mark(2, s);
   if (w.tc) {
@@ -293,9 +360,27 @@ int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, in
     BEAM_TRY(launch_down_simt(L, g, T, w.plan, w.act, w.opair, s));
     prof_mark(4, s);
   }
-  BEAM_TRY(launch_combine(w.plan, w.opair, w.tc ? BEAM_BF16 : BEAM_F32, T, g.Keff, g.d, g.d_pad, h, h_dtype, o->out, h_dtype, s));
+  BEAM_TRY(launch_combine(w.plan, w.opair, w.tc ? BEAM_BF16 : BEAM_F32, T, sp.Keff, g.d, g.d_pad, h, h_dtype, o->out, h_dtype, s));
   prof_mark(5, s);
   return BEAM_OK;
+}
+
+int beam_layer_forward(const beam_layer_t* layer, const void* h, int h_dtype, int T,
+                       int block_size, const beam_outputs_t* o, void* workspace,
+                       size_t workspace_bytes, beam_stream_t stream) {
+  return layer_forward(layer, nullptr, h, h_dtype, T, block_size, o, workspace, workspace_bytes, stream);
+}
+
+int beam_layer_forward_routed(const beam_layer_t* layer, const beam_route_t* route, const void* h,
+                              int h_dtype, int T, int block_size, const beam_outputs_t* o,
+                              void* workspace, size_t workspace_bytes, beam_stream_t stream) {
+  return layer_forward(layer, route, h, h_dtype, T, block_size, o, workspace, workspace_bytes, stream);
+}
+
+size_t beam_workspace_bytes_routed(const beam_layer_t* layer, const beam_route_t* route, int T, int block_size) {
+  Spec sp;
+  if (validate(layer) != BEAM_OK || T < 0 || spec_of(*layer, route, &sp) != BEAM_OK) return 0;
+  return carve(*layer, T, sp.Keff, block_size < 1 ? 1 : block_size, nullptr, nullptr, sp.cols);
 }
 
 int beam_gate(const beam_layer_t* layer, const void* h, int h_dtype, int T,
@@ -313,7 +398,9 @@ int beam_gate(const beam_layer_t* layer, const void* h, int h_dtype, int T,
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const void* X = nullptr;
   BEAM_TRY(strided_input(g, h, h_dtype, T, w, &X, s));
-  BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s));
+  Spec sp;
+  spec_of(L, nullptr, &sp);
+  BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s, sp));
   return BEAM_OK;
 }
 

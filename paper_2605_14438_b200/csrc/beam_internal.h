@@ -48,6 +48,12 @@ struct PlanDev {
 struct TopkArgs {
   int N, K, S;  // routed experts, top-k, shared experts (always-on slots K..K+S-1)
   float thr;    // keep iff a >= thr
+  // routing rule (BEAM_ROUTE_*) and its projection layout: router logits in
+  // columns [0, Nr) of a row of `cols` partials, mask pre-activations at mask_off
+  // (-1: none)
+  int kind = BEAM_ROUTE_BEAM, Nr = 0, cols = 0, mask_off = 0;
+  float phi = 0.5f, temp_inv = 1.0f, tau = 0.5f;
+  int binarize = 1;
   int has_norm, d, d_pad;
   float* inv_out;  // [T] inverse RMS (for the expert kernels)
   int32_t* ids32;  // [T, K+S] masked ids (int32), -1 = dropped

@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(128) topk_mask_kernel(const float* __restrict_
 template <typename TX>
 static void topk_dispatch(const float* L, int splits, const void* X, int T, const TopkArgs& a, cudaStream_t s) {
   const int grid = ceil_div(T, 4);
-  const int npl = ceil_div(a.N, 32);
+  const int npl = ceil_div(a.Nr, 32);
   if (npl <= 1) topk_mask_kernel<TX, 1><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
   else if (npl <= 2) topk_mask_kernel<TX, 2><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
   else if (npl <= 4) topk_mask_kernel<TX, 4><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   extern __shared__ float xs[];  // phase 1: token tile; phase 3: permute scratch
   __shared__ float red_s[8 * kGemvCols * kFusedTT];
   __shared__ int s_last;
-  const int cols = 2 * a.N;
+  const int cols = a.cols;
   trace_minmax(0, 1);
   router_gemv_body<TX, kFusedTT>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s);
   trace_minmax(2, 3);
@@ -426,12 +426,12 @@ static cudaError_t fused_launch(dim3 grid, size_t smem, const void* X, const flo
 cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, const float* gate_wT, int T,
                               int d, int d_pad, float* P, const TopkArgs& a, int E, int bs,
                               bool pad, const PlanDev& p, int* counters, cudaStream_t s) {
-  const int cols = 2 * a.N;
+  const int cols = a.cols;
   const int kr = gemv_kr(T, cols, d_pad, kFusedMaxSplit, kFusedTT);
   dim3 grid(ceil_div(cols, 8 * kGemvCols), ceil_div(d_pad, kr), ceil_div(T, kFusedTT));
   if ((int)grid.y > kFusedMaxSplit || (int)grid.z > kCounterSlots - 1) return cudaErrorInvalidValue;
   const size_t smem = std::max((size_t)kFusedTT * kr * sizeof(float), (size_t)(8 * E + 2 * E + 1 + 32) * sizeof(int));
-  const int npl = ceil_div(a.N, 32);
+  const int npl = ceil_div(a.Nr, 32);
   cudaError_t e;
 #define BEAM_FUSED(TX_)                                                                                        \
   if (npl <= 1) e = fused_launch<TX_, 1>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \

@@ -41,13 +41,22 @@ __device__ __forceinline__ T ld_maybe_cg(const T* p) {
 }
 
 
-// One warp, one token.  L = projection partials [splits][T][2N] (router then mask
-// columns), X = the token rows (stride d_pad) for inv_rms.  NPL = ceil(N / 32).
+// One warp, one token.  L = projection partials [splits][T][a.cols]: router
+// logits in columns [0, Nr), mask pre-activations (if any) in [mask_off,
+// mask_off + N); X = the token rows (stride d_pad) for inv_rms.  NPL = ceil(Nr / 32).
+// a.kind selects the routing rule (baselines.py:158-283, inference branch):
+//   BEAM     keep iff a >= thr, ghat = g * m                    (beam.py:127-165)
+//   TOPK     keep every candidate (vanilla / reduced / pruning: K = k_eff)
+//   DYNAMIC  p = softmax over all N; keep the shortest descending prefix with
+//            mass >= phi (dynamic_select, baselines.py:132-143); ghat = p / mass
+//   ADA      top-K over N real + null columns, keep the real ones, ghat = g
+//   SOFT     s = sigmoid(a / temp); binarize: keep iff s >= tau, ghat = g * keep;
+//            else keep all, ghat = g * s
 template <typename TX, int NPL, int MAXSPLIT, bool CG>
 __device__ __forceinline__ void topk_token(const float* __restrict__ L, int splits, int T,
                                            const TX* __restrict__ X, int t, int lane,
                                            const TopkArgs& a) {
-  const int N = a.N, K = a.K, Keff = a.K + a.S;
+  const int N = a.N, Nr = a.Nr, K = a.K, Keff = a.K + a.S;
   float inv = 1.0f;
   if (a.has_norm) {  // tensor.py:485-487: (mean(x^2) + eps)^-1/2 over the real d entries
     const TX* row = X + (size_t)t * a.d_pad;
@@ -65,8 +74,8 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
   }
   if (a.inv_out && lane == 0) a.inv_out[t] = inv;
 
-  // router logits v / mask pre-activations av of this lane's experts j = lane + 32 i,
-  // summed over the split-K partials in split order (all loads issued together)
+  // router logits v / mask pre-activations av of this lane's columns j = lane + 32 i,
+  // summed over the split-K partials in split order
   float v[NPL], av[NPL];
   int rank[NPL];
 #pragma unroll
@@ -75,7 +84,8 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
     av[i] = 0.0f;
     rank[i] = -1;
   }
-  // Loads are unconditional (clamped split / expert index, masked add) and issued
+  const bool has_mask = a.mask_off >= 0;
+  // Loads are unconditional (clamped split / column index, masked add) and issued
   // four splits at a time: conditional loads inside the unrolled loop would be
   // serialised, one L2 round trip each.  The sum runs in split order.
   constexpr int kSB = MAXSPLIT < 4 ? MAXSPLIT : 4;
@@ -85,12 +95,11 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
       float pv[kSB][NPL], pa[kSB][NPL];
 #pragma unroll
       for (int q = 0; q < kSB; ++q) {
-        const float* row = L + ((size_t)min(sp0 + q, splits - 1) * T + t) * 2 * N;
+        const float* row = L + ((size_t)min(sp0 + q, splits - 1) * T + t) * a.cols;
 #pragma unroll
         for (int i = 0; i < NPL; ++i) {
-          const int j = min(lane + 32 * i, N - 1);
-          pv[q][i] = ld_maybe_cg<CG>(row + j);
-          pa[q][i] = ld_maybe_cg<CG>(row + N + j);
+          pv[q][i] = ld_maybe_cg<CG>(row + min(lane + 32 * i, Nr - 1));
+          pa[q][i] = has_mask ? ld_maybe_cg<CG>(row + a.mask_off + min(lane + 32 * i, N - 1)) : 0.0f;
         }
       }
 #pragma unroll
@@ -110,17 +119,16 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
     av[i] *= inv;
   }
 
-  // Selection on 64-bit keys (order-preserving float bits << 32 | ~expert id):
-  // one max per butterfly level, and the key order is exactly the reference's
-  // (value desc, ties -> lower id, moe.py:116-119); NaN logits rank last.
-  // K rounds of a 5-level butterfly, one 64-bit shuffle per level.
+  // Selection on 64-bit keys (order-preserving float bits << 32 | ~column): one
+  // max per butterfly level, and the key order is exactly the reference's
+  // (value desc, ties -> lower index, moe.py:116-119); NaN logits rank last.
   unsigned long long key[NPL];
 #pragma unroll
   for (int i = 0; i < NPL; ++i) {
     const int j = lane + 32 * i;
     const unsigned fb = __float_as_uint(v[i]);
     const unsigned ord = v[i] != v[i] ? 0u : ((fb & 0x80000000u) ? ~fb : (fb | 0x80000000u));
-    key[i] = j < N ? (((unsigned long long)ord << 32) | (unsigned)(~j)) : 0ull;
+    key[i] = j < Nr ? (((unsigned long long)ord << 32) | (unsigned)(~j)) : 0ull;
   }
   int top_j = 0;
   for (int r = 0; r < K; ++r) {
@@ -141,41 +149,110 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
         key[i] = 0ull;
       }
   }
-  // the top logit (softmax shift) from the lane that holds expert top_j
+  // the top logit (softmax shift) from the lane that holds column top_j
   float mine = 0.0f;
 #pragma unroll
   for (int i = 0; i < NPL; ++i)
     if (lane + 32 * i == top_j) mine = v[i];
   const float top_val = __shfl_sync(0xffffffffu, mine, top_j & 31);
 
-  // softmax over the K kept logits (tensor.py:440-451): exp(l - max) / sum
+  // softmax over the K kept logits (tensor.py:440-451): exp(l - max) / sum;
+  // DYNAMIC: softmax over all N columns (baselines.py:191-192)
+  const bool dyn = a.kind == BEAM_ROUTE_DYNAMIC;
   float part = 0.0f;
 #pragma unroll
   for (int i = 0; i < NPL; ++i)
-    if (rank[i] >= 0) part += expf(v[i] - top_val);
+    if (dyn ? (lane + 32 * i < Nr) : (rank[i] >= 0)) part += expf(v[i] - top_val);
   const float denom = warp_sum(part);
+
+  // DYNAMIC: the kept prefix — count = #(cumulative mass < phi) + 1 over the
+  // descending order (dynamic_select); ranks < K suffice unless the K most
+  // probable experts hold less than phi (the reference then plans more slots
+  // than candidates and its grouped_execute raises ContractError)
+  int count = K;
+  float kept_mass = 1.0f;
+  if (dyn) {
+    // p of rank r -> lane r (the owner of rank r is found with a ballot)
+    float p_rank = 0.0f;
+    for (int r = 0; r < K; ++r) {
+      float cand = 0.0f;
+      bool mine_r = false;
+#pragma unroll
+      for (int i = 0; i < NPL; ++i)
+        if (rank[i] == r) {
+          cand = expf(v[i] - top_val) / denom;
+          mine_r = true;
+        }
+      const unsigned owner = __ballot_sync(0xffffffffu, mine_r);
+      const float pv = __shfl_sync(0xffffffffu, cand, __ffs(owner) - 1);
+      if (lane == r) p_rank = pv;
+    }
+    // inclusive scan of p over ranks 0..K-1 (sequential order: csum is a running sum)
+    float csum = p_rank;
+    for (int o = 1; o < 32; o <<= 1) {
+      const float y = __shfl_up_sync(0xffffffffu, csum, o);
+      if (lane >= o) csum += y;
+    }
+    const unsigned below = __ballot_sync(0xffffffffu, lane < K && csum < a.phi);
+    count = min(__popc(below) + 1, Nr);
+    const float mass = __shfl_sync(0xffffffffu, csum, min(count, K) - 1);
+    kept_mass = mass;
+  }
 
 #pragma unroll
   for (int i = 0; i < NPL; ++i) {
     const int j = lane + 32 * i;
-    if (j >= N) continue;
+    if (j >= Nr) continue;
     const float x = av[i];
-    const bool keep = x >= a.thr;  // NaN -> false
-    const float g = rank[i] >= 0 ? expf(v[i] - top_val) / denom : 0.0f;
+    const float e = expf(v[i] - top_val) / denom;  // softmax value of this column
+    const float g = (dyn || rank[i] >= 0) ? e : 0.0f;
+    bool keep;
+    float w, mval = 1.0f, sval = 0.0f;
+    switch (a.kind) {
+      case BEAM_ROUTE_TOPK:
+        keep = true;
+        w = g;
+        break;
+      case BEAM_ROUTE_DYNAMIC:
+        keep = rank[i] >= 0 && rank[i] < count;
+        w = keep ? g / kept_mass : 0.0f;
+        break;
+      case BEAM_ROUTE_ADA:
+        keep = j < N;
+        w = keep ? g : 0.0f;
+        break;
+      case BEAM_ROUTE_SOFT:
+        sval = sigmoid_ref(x * a.temp_inv);
+        mval = sval >= a.tau ? 1.0f : 0.0f;  // NaN -> 0
+        keep = a.binarize ? mval != 0.0f : true;
+        w = a.binarize ? g * mval : g * sval;
+        break;
+      default:  // BEAM
+        keep = x >= a.thr;  // NaN -> false
+        mval = keep ? 1.0f : 0.0f;
+        w = keep ? g : 0.0f;
+        sval = sigmoid_ref(x);
+        break;
+    }
     if (rank[i] >= 0) {
       const int r = rank[i];
       const size_t o = (size_t)t * Keff + r;
       a.ids32[o] = keep ? j : -1;
-      a.gw[o] = keep ? g : 0.0f;
-      if (a.topk_ids) a.topk_ids[(size_t)t * K + r] = j;
+      a.gw[o] = keep ? w : 0.0f;
+      if (a.topk_ids) a.topk_ids[(size_t)t * K + r] = (a.kind == BEAM_ROUTE_ADA && j >= N) ? -1 : j;
       if (a.masked_ids) a.masked_ids[(size_t)t * K + r] = keep ? j : -1;
     }
-    const size_t od = (size_t)t * N + j;
-    if (a.logits) a.logits[od] = v[i];
-    if (a.weights) a.weights[od] = g;
-    if (a.pre_act) a.pre_act[od] = x;
-    if (a.raw_mask) a.raw_mask[od] = sigmoid_ref(x);
-    if (a.mask) a.mask[od] = keep ? 1.0f : 0.0f;
+    if (a.logits) a.logits[(size_t)t * Nr + j] = v[i];
+    if (j < N) {
+      const size_t od = (size_t)t * N + j;
+      // RouterDecision.weights (BEAM) / RouteResult.weights_hat (other rules)
+      if (a.weights) a.weights[od] = a.kind == BEAM_ROUTE_BEAM ? g : (rank[i] >= 0 && keep ? w : 0.0f);
+      if (has_mask) {
+        if (a.pre_act) a.pre_act[od] = x;
+        if (a.raw_mask) a.raw_mask[od] = sval;
+        if (a.mask) a.mask[od] = mval;
+      }
+    }
   }
   // shared experts: always-on slots K..K+S-1, weight 1.0 (beam.py:163-164)
   for (int s = lane; s < a.S; s += 32) {

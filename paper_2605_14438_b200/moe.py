@@ -185,8 +185,8 @@ class MoEBlock:
     def __init__(self, cfg: MoEBlockConfig, rng: np.random.Generator | None = None,
                  extra_router_cols: int = 0, init_std: float = 0.02, *,
                  dtype: torch.dtype = torch.bfloat16, device=None, _empty: bool = False):
-        if extra_router_cols:
-            raise ContractError("extra router columns (null-expert routing) are not part of the BEAM path")
+        if extra_router_cols < 0:
+            raise ContractError("extra_router_cols must be >= 0")
         if dtype not in (torch.bfloat16, torch.float32):
             raise ContractError("expert dtype must be torch.bfloat16 or torch.float32")
         self.cfg = cfg
@@ -195,7 +195,11 @@ class MoEBlock:
         n_all = cfg.num_experts + cfg.num_shared
         self.w_gu = torch.zeros(n_all, 2 * cfg.f_pad, cfg.d_pad, dtype=dtype, device=self.device)
         self.w_down = torch.zeros(n_all, cfg.d_pad, cfg.f_pad, dtype=dtype, device=self.device)
-        self.router_w = torch.zeros(cfg.d_h, cfg.num_experts, dtype=torch.float32, device=self.device)
+        # moe.py:164-178: num_experts + extra_router_cols columns (the extra ones are the
+        # null experts of ada_moe routing, baselines.py:212-225)
+        self.extra_router_cols = extra_router_cols
+        self.router_w = torch.zeros(cfg.d_h, cfg.num_experts + extra_router_cols, dtype=torch.float32,
+                                    device=self.device)
         self.norm_w = torch.ones(cfg.d_h, dtype=torch.float32, device=self.device) if cfg.has_norm else None
         self._mask_router = None
         self._pack_key = None
@@ -204,7 +208,8 @@ class MoEBlock:
             return
         rng = rng if rng is not None else np.random.default_rng()
         # moe.py:177-191: router, experts (gate, up, down each), shared — same draws
-        self.router_w.copy_(torch.from_numpy(rng.normal(0.0, init_std, (cfg.d_h, cfg.num_experts))))
+        self.router_w.copy_(torch.from_numpy(
+            rng.normal(0.0, init_std, (cfg.d_h, cfg.num_experts + extra_router_cols))))
         for i in range(n_all):
             self._set_expert(i, Expert.init_random(cfg.d_h, cfg.d_ff, rng, init_std))
 
@@ -217,8 +222,12 @@ class MoEBlock:
         stacked [E, d, f]/[E, d, f]/[E, f, d] tensors (3-tuple of 3-D arrays)."""
         from .beam import MaskRouter
 
-        b = cls(cfg, dtype=dtype, device=device, _empty=True)
-        b.router_w.copy_(as_torch(router_w).to(torch.float32))
+        rw = as_torch(router_w)
+        extra = rw.shape[-1] - cfg.num_experts
+        if rw.ndim != 2 or rw.shape[0] != cfg.d_h or extra < 0:
+            raise ShapeError("router_w must be [d_h, num_experts (+ null columns)]")
+        b = cls(cfg, extra_router_cols=extra, dtype=dtype, device=device, _empty=True)
+        b.router_w.copy_(rw.to(torch.float32))
         if norm_w is not None and b.norm_w is not None:
             b.norm_w.copy_(as_torch(norm_w).to(torch.float32))
         b._set_all_experts(experts, 0, cfg.num_experts)
@@ -325,15 +334,18 @@ class MoEBlock:
                self.norm_w._version if self.norm_w is not None else -1)
         if key != self._pack_key:
             # repacked in place: captured CUDA graphs keep a valid pointer
+            # rows: router [N (+ null columns)], mask router at rows [N, 2N) (beam_route_t)
+            nr = self.router_w.shape[1]
             if getattr(self, "gate_wT", None) is None:
-                self.gate_wT = torch.zeros(2 * cfg.num_experts, cfg.d_pad, dtype=torch.float32,
+                self.gate_wT = torch.zeros(max(2 * cfg.num_experts, nr), cfg.d_pad, dtype=torch.float32,
                                            device=self.device)
             gate = self.gate_wT
-            gate[: cfg.num_experts, : cfg.d_h] = self.router_w.t()
+            gate.zero_()
+            gate[:nr, : cfg.d_h] = self.router_w.t()
             if mw is not None:
-                gate[cfg.num_experts :, : cfg.d_h] = mw.t()
-            else:
-                gate[cfg.num_experts :].zero_()
+                if nr > cfg.num_experts:
+                    raise ContractError("a block with null-expert router columns has no mask router")
+                gate[cfg.num_experts : 2 * cfg.num_experts, : cfg.d_h] = mw.t()
             self._pack_key = key
         ck = (key, mask_threshold, id(self.norm_w), id(self.w_gu), id(self.w_down), id(self.gate_wT))
         cached = getattr(self, "_desc_cache", None)

@@ -15,6 +15,8 @@ align_*           — dispatch.align_block (dispatch/__init__.py:89-126), many b
 topk_*            — moe.topk_route incl. ties (moe.py:116-137)
 layer_*           — beam.beam_block_forward(training=False) (beam.py:127-165)
                     on small random blocks (norm / shared / non-zero mask router)
+strategies        — baselines.block_forward(training=False) (baselines.py:286-323) for every
+                    routing strategy (top-k variants, moe_dynamic, ada_moe, beam, soft masks)
 q30route_dyadic   — Qwen3-30B-A3B router shape (N=128, K=8, d=2048), dyadic inputs,
                     so logits / pre-activations are exact in fp32 and fp64: top-K ids,
                     mask bits and the plan must match bit-for-bit.
@@ -50,7 +52,70 @@ def save(name, **arrays):
     print(f"wrote {path} ({os.path.getsize(path)} bytes)")
 
 
+def make_strategies():
+    """Every routing strategy of baselines.route through block_forward(training=False)."""
+    ref.import_beamoe()
+    from beamoe import baselines
+    from beamoe.moe import MoEBlockConfig
+    from beamoe.tensor import Tensor
+
+    specs = [
+        # (seed, kind, params, binarize_soft, d, f, n, k, shared, has_norm, T, mask_std)
+        (21, "vanilla_topk", {}, False, 32, 24, 8, 2, 0, True, 29, 0.0),
+        (22, "topk_reduced", {"k_small": 1}, False, 32, 24, 8, 3, 0, True, 31, 0.0),
+        (23, "topk_pruning", {"k_infer": 2}, False, 32, 24, 8, 4, 1, True, 17, 0.0),
+        (24, "moe_dynamic", {"phi": 0.3}, False, 32, 24, 8, 4, 0, True, 40, 0.0),
+        (25, "ada_moe", {"null_count": 3}, False, 32, 24, 8, 3, 0, True, 35, 0.0),
+        (26, "beam", {"tau": 0.5}, False, 32, 24, 8, 3, 0, True, 33, 1.0),
+        (27, "soft_mask", {"tau": 0.5}, False, 32, 24, 8, 3, 0, True, 27, 1.0),
+        (28, "soft_mask", {"tau": 0.5}, True, 32, 24, 8, 3, 0, False, 25, 1.0),
+        (29, "soft_mask_tempered", {"tau": 0.5, "temp_floor": 0.2}, False, 32, 24, 8, 3, 1, True, 21, 1.0),
+    ]
+    arrays = {}
+    for i, (seed, kind, params, bsoft, d, f, n, k, sh, norm, t, mstd) in enumerate(specs):
+        rng = np.random.default_rng(seed)
+        cfg = MoEBlockConfig(d_h=d, d_ff=f, num_experts=n, top_k=k, num_shared=sh, has_norm=norm)
+        strat = baselines.RoutingStrategy(kind, dict(params))
+        block = baselines.build_block(cfg, strat, rng)
+        for e in list(block.experts) + list(block.shared):  # larger weights: visible outputs
+            for w in (e.w_gate, e.w_up, e.w_down):
+                w.data[...] = rng.normal(0, 0.3, w.data.shape)
+        if block.mask_router is not None and mstd > 0:
+            block.mask_router.weight.data[...] = rng.normal(0, mstd, (d, n))
+        h = rng.normal(size=(t, d))
+        out, rr = baselines.block_forward(Tensor(h), block, strat, training=False, binarize_soft=bsoft,
+                                          block_size=4)
+        p = f"c{i}_"
+        arrays[p + "cfg"] = np.array([seed, d, f, n, k, sh, int(norm), t, int(bsoft)], np.int64)
+        arrays[p + "kind"] = np.array(kind)
+        for key, v in params.items():
+            arrays[p + "param_" + key] = np.float64(v)
+        arrays[p + "h"] = h
+        arrays[p + "router_w"] = block.router_w.data
+        if block.mask_router is not None:
+            arrays[p + "mask_w"] = block.mask_router.weight.data
+        arrays[p + "w_gate"] = np.stack([e.w_gate.data for e in block.experts])
+        arrays[p + "w_up"] = np.stack([e.w_up.data for e in block.experts])
+        arrays[p + "w_down"] = np.stack([e.w_down.data for e in block.experts])
+        if sh:
+            arrays[p + "s_gate"] = np.stack([e.w_gate.data for e in block.shared])
+            arrays[p + "s_up"] = np.stack([e.w_up.data for e in block.shared])
+            arrays[p + "s_down"] = np.stack([e.w_down.data for e in block.shared])
+        arrays[p + "out"] = out.data
+        arrays[p + "weights_hat"] = rr.weights_hat.data
+        arrays[p + "logits"] = rr.logits.data
+        arrays[p + "candidate_ids"] = rr.candidate_ids
+        arrays[p + "active_bits"] = rr.active_bits
+        arrays[p + "active_counts"] = rr.active_counts
+        arrays[p + "kept_ids"] = rr.kept_ids
+        if rr.raw_mask is not None:
+            arrays[p + "raw_mask"] = rr.raw_mask.data
+    arrays["n_cases"] = np.int64(len(specs))
+    save("strategies", **arrays)
+
+
 def main():
+    make_strategies()
     beamoe = ref.import_beamoe()
     from beamoe import dispatch
     from beamoe.beam import MaskRouter, beam_block_forward
