@@ -363,7 +363,7 @@ def run_ours(args):
     from paper_2605_14438_b200 import _lib
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    if world > 1 or os.environ.get("BEAM_BENCH_FORCE_EP") == "1":  # the EP path (forced: 1-rank check)
         from paper_2605_14438_b200 import ep
 
         return ep.bench_main(args, sys.modules[__name__])

@@ -295,23 +295,31 @@ cudaError_t launch_router(const void* X, int x_dtype, const float* norm_w, const
 // ---------------------------------------------------------------------------
 // 3. Stand-alone top-K + softmax + mask (prefill / wide N): one warp per token.
 // ---------------------------------------------------------------------------
-template <typename TX, int NPL>
+template <typename TX, int NPL, int KIND>
 __global__ void __launch_bounds__(128) topk_mask_kernel(const float* __restrict__ L, int splits,
                                                         const TX* __restrict__ X, int T, TopkArgs a) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (t >= T) return;
-  topk_token<TX, NPL, 16, false>(L, splits, T, X, t, threadIdx.x & 31, a);
+  topk_token<TX, NPL, 16, false, KIND>(L, splits, T, X, t, threadIdx.x & 31, a);
+}
+
+template <typename TX, int KIND>
+static void topk_dispatch_k(const float* L, int splits, const void* X, int T, const TopkArgs& a, cudaStream_t s) {
+  const int grid = ceil_div(T, 4);
+  const int npl = ceil_div(a.Nr, 32);
+  if (npl <= 1) topk_mask_kernel<TX, 1, KIND><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
+  else if (npl <= 2) topk_mask_kernel<TX, 2, KIND><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
+  else if (npl <= 4) topk_mask_kernel<TX, 4, KIND><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
+  else if (npl <= 8) topk_mask_kernel<TX, 8, KIND><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
+  else topk_mask_kernel<TX, 16, KIND><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
 }
 
 template <typename TX>
 static void topk_dispatch(const float* L, int splits, const void* X, int T, const TopkArgs& a, cudaStream_t s) {
-  const int grid = ceil_div(T, 4);
-  const int npl = ceil_div(a.Nr, 32);
-  if (npl <= 1) topk_mask_kernel<TX, 1><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
-  else if (npl <= 2) topk_mask_kernel<TX, 2><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
-  else if (npl <= 4) topk_mask_kernel<TX, 4><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
-  else if (npl <= 8) topk_mask_kernel<TX, 8><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
-  else topk_mask_kernel<TX, 16><<<grid, 128, 0, s>>>(L, splits, (const TX*)X, T, a);
+  if (a.kind == BEAM_ROUTE_BEAM && a.Nr == a.N && a.cols == 2 * a.N && a.mask_off == a.N)
+    topk_dispatch_k<TX, BEAM_ROUTE_BEAM>(L, splits, X, T, a, s);
+  else
+    topk_dispatch_k<TX, -1>(L, splits, X, T, a, s);
 }
 
 cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dtype, int T,
@@ -356,7 +364,7 @@ __device__ __forceinline__ void trace_minmax(int lo, int hi) {
 }
 constexpr int kCounterSlots = 16;  // [0, 8) token tiles, [15] tiles-done
 
-template <typename TX, int NPL>
+template <typename TX, int NPL, int KIND>
 __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ X, const float* __restrict__ nw,
                                                          const float* __restrict__ W, int T, int d, int d_pad,
                                                          int kr, float* __restrict__ P, TopkArgs a, int E,
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   const int t0 = tile * kFusedTT, nt = min(kFusedTT, T - t0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int t = t0 + warp; t < t0 + nt; t += 8)
-    topk_token<TX, NPL, kFusedMaxSplit, true>(P, gridDim.y, T, X, t, lane, a);
+    topk_token<TX, NPL, kFusedMaxSplit, true, KIND>(P, gridDim.y, T, X, t, lane, a);
   if (threadIdx.x == 0) counters[tile] = 0;
   __syncthreads();
   trace_minmax(-1, 4);
@@ -410,16 +418,16 @@ bool gate_fused_supported(int T, int N, int E, int d_pad) {
   return T >= 1 && T <= 64 && N <= 512 && E <= 256 && d_pad % 4 == 0;
 }
 
-template <typename TX, int NPL>
+template <typename TX, int NPL, int KIND>
 static cudaError_t fused_launch(dim3 grid, size_t smem, const void* X, const float* nw, const float* W, int T,
                                 int d, int d_pad, int kr, float* P, const TopkArgs& a, int E, int bs,
                                 bool pad, const PlanDev& p, int* counters, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    set_smem(gate_fused_kernel<TX, NPL>, 160 * 1024);
+    set_smem(gate_fused_kernel<TX, NPL, KIND>, 160 * 1024);
     attr = true;
   }
-  gate_fused_kernel<TX, NPL><<<grid, 256, smem, s>>>((const TX*)X, nw, W, T, d, d_pad, kr, P, a, E, bs, pad, p, counters);
+  gate_fused_kernel<TX, NPL, KIND><<<grid, 256, smem, s>>>((const TX*)X, nw, W, T, d, d_pad, kr, P, a, E, bs, pad, p, counters);
   return cudaGetLastError();
 }
 
@@ -433,16 +441,17 @@ cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, c
   const size_t smem = std::max((size_t)kFusedTT * kr * sizeof(float), (size_t)(8 * E + 2 * E + 1 + 32) * sizeof(int));
   const int npl = ceil_div(a.Nr, 32);
   cudaError_t e;
-#define BEAM_FUSED(TX_)                                                                                        \
-  if (npl <= 1) e = fused_launch<TX_, 1>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
-  else if (npl <= 2) e = fused_launch<TX_, 2>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
-  else if (npl <= 4) e = fused_launch<TX_, 4>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
-  else if (npl <= 8) e = fused_launch<TX_, 8>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
-  else e = fused_launch<TX_, 16>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s);
+#define BEAM_FUSED(TX_, K_)                                                                                    \
+  if (npl <= 1) e = fused_launch<TX_, 1, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
+  else if (npl <= 2) e = fused_launch<TX_, 2, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
+  else if (npl <= 4) e = fused_launch<TX_, 4, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
+  else if (npl <= 8) e = fused_launch<TX_, 8, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
+  else e = fused_launch<TX_, 16, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s);
+  const bool beam = a.kind == BEAM_ROUTE_BEAM && a.Nr == a.N && a.cols == 2 * a.N && a.mask_off == a.N;
   if (x_dtype == BEAM_BF16) {
-    BEAM_FUSED(__nv_bfloat16)
+    if (beam) { BEAM_FUSED(__nv_bfloat16, BEAM_ROUTE_BEAM) } else { BEAM_FUSED(__nv_bfloat16, -1) }
   } else {
-    BEAM_FUSED(float)
+    if (beam) { BEAM_FUSED(float, BEAM_ROUTE_BEAM) } else { BEAM_FUSED(float, -1) }
   }
 #undef BEAM_FUSED
   count_launches(1);

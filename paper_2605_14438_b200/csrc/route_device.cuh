@@ -52,11 +52,14 @@ __device__ __forceinline__ T ld_maybe_cg(const T* p) {
 //   ADA      top-K over N real + null columns, keep the real ones, ghat = g
 //   SOFT     s = sigmoid(a / temp); binarize: keep iff s >= tau, ghat = g * keep;
 //            else keep all, ghat = g * s
-template <typename TX, int NPL, int MAXSPLIT, bool CG>
+// KIND >= 0 fixes the rule at compile time (the BEAM hot path carries none of
+// the other rules' code); KIND = -1 reads a.kind.
+template <typename TX, int NPL, int MAXSPLIT, bool CG, int KIND = -1>
 __device__ __forceinline__ void topk_token(const float* __restrict__ L, int splits, int T,
                                            const TX* __restrict__ X, int t, int lane,
                                            const TopkArgs& a) {
-  const int N = a.N, Nr = a.Nr, K = a.K, Keff = a.K + a.S;
+  const int N = a.N, Nr = KIND == BEAM_ROUTE_BEAM ? a.N : a.Nr, K = a.K, Keff = a.K + a.S;
+  const int kind = KIND >= 0 ? KIND : a.kind;
   float inv = 1.0f;
   if (a.has_norm) {  // tensor.py:485-487: (mean(x^2) + eps)^-1/2 over the real d entries
     const TX* row = X + (size_t)t * a.d_pad;
@@ -84,7 +87,9 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
     av[i] = 0.0f;
     rank[i] = -1;
   }
-  const bool has_mask = a.mask_off >= 0;
+  const bool has_mask = KIND == BEAM_ROUTE_BEAM ? true : a.mask_off >= 0;
+  const int cols = KIND == BEAM_ROUTE_BEAM ? 2 * a.N : a.cols;
+  const int mask_off = KIND == BEAM_ROUTE_BEAM ? a.N : a.mask_off;
   // Loads are unconditional (clamped split / column index, masked add) and issued
   // four splits at a time: conditional loads inside the unrolled loop would be
   // serialised, one L2 round trip each.  The sum runs in split order.
@@ -95,11 +100,11 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
       float pv[kSB][NPL], pa[kSB][NPL];
 #pragma unroll
       for (int q = 0; q < kSB; ++q) {
-        const float* row = L + ((size_t)min(sp0 + q, splits - 1) * T + t) * a.cols;
+        const float* row = L + ((size_t)min(sp0 + q, splits - 1) * T + t) * cols;
 #pragma unroll
         for (int i = 0; i < NPL; ++i) {
           pv[q][i] = ld_maybe_cg<CG>(row + min(lane + 32 * i, Nr - 1));
-          pa[q][i] = has_mask ? ld_maybe_cg<CG>(row + a.mask_off + min(lane + 32 * i, N - 1)) : 0.0f;
+          pa[q][i] = has_mask ? ld_maybe_cg<CG>(row + mask_off + min(lane + 32 * i, N - 1)) : 0.0f;
         }
       }
 #pragma unroll
@@ -158,7 +163,7 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
 
   // softmax over the K kept logits (tensor.py:440-451): exp(l - max) / sum;
   // DYNAMIC: softmax over all N columns (baselines.py:191-192)
-  const bool dyn = a.kind == BEAM_ROUTE_DYNAMIC;
+  const bool dyn = kind == BEAM_ROUTE_DYNAMIC;
   float part = 0.0f;
 #pragma unroll
   for (int i = 0; i < NPL; ++i)
@@ -208,7 +213,7 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
     const float g = (dyn || rank[i] >= 0) ? e : 0.0f;
     bool keep;
     float w, mval = 1.0f, sval = 0.0f;
-    switch (a.kind) {
+    switch (kind) {
       case BEAM_ROUTE_TOPK:
         keep = true;
         w = g;
@@ -239,14 +244,14 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
       const size_t o = (size_t)t * Keff + r;
       a.ids32[o] = keep ? j : -1;
       a.gw[o] = keep ? w : 0.0f;
-      if (a.topk_ids) a.topk_ids[(size_t)t * K + r] = (a.kind == BEAM_ROUTE_ADA && j >= N) ? -1 : j;
+      if (a.topk_ids) a.topk_ids[(size_t)t * K + r] = (kind == BEAM_ROUTE_ADA && j >= N) ? -1 : j;
       if (a.masked_ids) a.masked_ids[(size_t)t * K + r] = keep ? j : -1;
     }
     if (a.logits) a.logits[(size_t)t * Nr + j] = v[i];
     if (j < N) {
       const size_t od = (size_t)t * N + j;
       // RouterDecision.weights (BEAM) / RouteResult.weights_hat (other rules)
-      if (a.weights) a.weights[od] = a.kind == BEAM_ROUTE_BEAM ? g : (rank[i] >= 0 && keep ? w : 0.0f);
+      if (a.weights) a.weights[od] = kind == BEAM_ROUTE_BEAM ? g : (rank[i] >= 0 && keep ? w : 0.0f);
       if (has_mask) {
         if (a.pre_act) a.pre_act[od] = x;
         if (a.raw_mask) a.raw_mask[od] = sval;

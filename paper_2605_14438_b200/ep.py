@@ -189,24 +189,46 @@ def bench_main(args, bench):
     blk.w_down = torch.zeros(1, dtype=torch.bfloat16, device=dev)
     x = h.to(dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    lib = _lib.load()
     for _ in range(args.warmup):
         layer.forward(x)
     torch.cuda.synchronize()
+    c0 = lib.beam_kernel_launches()
+    layer.forward(x)  # launches of one step through the C ABI (gate + local experts)
+    torch.cuda.synchronize()
+    launches_per_step = int(lib.beam_kernel_launches() - c0)
     dist.barrier()
     total = 0.0
+    with bench.ClockSampler(dev.index) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            layer.forward(x)
+            e.record()
+            e.synchronize()
+            total += s.elapsed_time(e)
+    t_max = torch.tensor([total], device=dev)
+    dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item()) / args.steps
+    # e2e: pinned host tokens -> device -> EP layer -> host output, every step
+    h_pin = h.pin_memory()
+    out_host = torch.empty(h.shape, dtype=h.dtype).pin_memory()
+    e2e_total = 0.0
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         dist.barrier()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        layer.forward(x)
-        e.record()
-        e.synchronize()
-        total += s.elapsed_time(e)
-    t_max = torch.tensor([total], device=dev)
-    dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms = float(t_max.item()) / args.steps
+        t0 = time.perf_counter()
+        y = layer.forward(h_pin.to(dev, non_blocking=True))
+        out_host.copy_(y, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_total += time.perf_counter() - t0
+    e2e_max = torch.tensor([e2e_total], device=dev)
+    dist.all_reduce(e2e_max, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_max.item()) / args.steps
     if rank == 0:
         line = {
             "metric": bench.METRIC, "value": world * args.tokens / (ms / 1e3), "unit": "tokens/s",
@@ -216,8 +238,16 @@ def bench_main(args, bench):
             "config": {"workload": f"Qwen3-30B-A3B MoE layer, expert parallel EP{world}, T={args.tokens} tokens/rank, "
                                    f"s={args.sparsity}", **q, "parallelism": f"ep{world}",
                        "experts_per_rank": q["n"] // world, "l2": "flushed before every step",
-                       "timing": "CUDA events per step, max over ranks"},
-            "gpu_launches": None,
+                       "timing": "CUDA events per step, max over ranks",
+                       "exchange": "NCCL all_to_all_single (counts, rows, metadata, partial sums)"},
+            "e2e": {"value": world * args.tokens / e2e_s, "unit": "tokens/s",
+                    "h2d_bytes_per_step": world * int(h.numel()) * h.element_size(),
+                    "d2h_bytes_per_step": world * int(h.numel()) * h.element_size(),
+                    "path": "EPBeamLayer.forward(pinned host tokens -> device) -> host output, max over ranks"},
+            "roofline": None,
+            "clocks": clocks.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches_per_step": launches_per_step,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
