@@ -24,12 +24,12 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, seed, t, n, k, out_q):
+def _worker(rank, world, port, seed, t, n, k, out_q, fixed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2605_14438_b200.ep import Gated, ep_exchange_forward
+        from paper_2605_14438_b200.ep import Gated, ep_exchange_forward, ep_exchange_forward_fixed
 
         rng = np.random.default_rng(seed)
         ob = O.make_block(16, 12, n, k, rng, init_std=0.3)
@@ -54,19 +54,21 @@ def _worker(rank, world, port, seed, t, n, k, out_q):
             return torch.from_numpy(y)
 
         g = Gated(xn=torch.from_numpy(xn), ids=torch.from_numpy(ids), ghat=torch.from_numpy(ghat).float().double())
-        out = ep_exchange_forward(torch.from_numpy(h), g, n, local_fn)
+        fwd = ep_exchange_forward_fixed if fixed else ep_exchange_forward
+        out = fwd(torch.from_numpy(h), g, n, local_fn)
         ref = O.beam_block_forward(h, ob).out
         out_q.put((rank, float(np.abs(out.numpy() - ref).max()), int((ids >= 0).sum())))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("seed,t,n,k", [(0, 9, 8, 2), (1, 17, 4, 4), (2, 1, 8, 3)])
-def test_ep2_matches_single_process(seed, t, n, k):
+@pytest.mark.parametrize("seed,t,n,k,fixed", [(0, 9, 8, 2, False), (1, 17, 4, 4, False), (2, 1, 8, 3, False),
+                                              (3, 9, 8, 2, True), (4, 1, 8, 3, True)])
+def test_ep2_matches_single_process(seed, t, n, k, fixed):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, seed, t, n, k, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, seed, t, n, k, q, fixed)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
