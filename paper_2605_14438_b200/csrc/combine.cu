@@ -47,27 +47,25 @@ __global__ void __launch_bounds__(32 * kCombineWarps, 3) combine_kernel(const in
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * kCombineWarps + (threadIdx.x >> 5);
   if (t >= T) return;
-  // lane k < Keff holds slot k; rank = number of surviving slots with a smaller
-  // (expert, slot) key -> the sorted position list, broadcast by shuffles
-  int e = -1, pos = -1;
-  if (lane < Keff) {
-    pos = slot_pos[(size_t)t * Keff + lane];
-    e = pos >= 0 ? slot_expert[(size_t)t * Keff + lane] : -1;
-  }
+  // lane k < Keff holds slot k.  Plan positions are laid out by ascending expert
+  // (then ascending flat index), and a token meets each expert once, so ascending
+  // position == the reference's ascending-expert order: rank = number of surviving
+  // slots with a smaller position (no second, dependent load of the slot's expert)
+  int pos = -1;
+  if (lane < Keff) pos = slot_pos[(size_t)t * Keff + lane];
   int rank = 0, nv = 0;
 #pragma unroll 4
   for (int j = 0; j < min(Keff, 32); ++j) {
-    const int ej = __shfl_sync(0xffffffffu, e, j);
-    nv += ej >= 0;
-    rank += ej >= 0 && e >= 0 && (ej < e || (ej == e && j < lane));
+    const int pj = __shfl_sync(0xffffffffu, pos, j);
+    nv += pj >= 0;
+    rank += pj >= 0 && pos >= 0 && pj < pos;
   }
   // sorted[r] = pos of the slot with rank r (r < nv)
   int sorted_pos = -1;
   for (int j = 0; j < min(Keff, 32); ++j) {
     const int rj = __shfl_sync(0xffffffffu, rank, j);
     const int pj = __shfl_sync(0xffffffffu, pos, j);
-    const int ej = __shfl_sync(0xffffffffu, e, j);
-    if (ej >= 0 && rj == lane) sorted_pos = pj;
+    if (pj >= 0 && rj == lane) sorted_pos = pj;
   }
   {
     const int c0 = blockIdx.y * 256 + 8 * lane;
