@@ -93,6 +93,12 @@ __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.
 // warp reductions
 // ---------------------------------------------------------------------------
 
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

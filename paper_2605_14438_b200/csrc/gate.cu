@@ -393,6 +393,14 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   if (threadIdx.x == 0) counters[tile] = 0;
   __syncthreads();
   trace_minmax(-1, 4);
+  if (gridDim.z == 1 && T * (a.K + a.S) <= 32) {
+    // one token tile and <= 32 slots: this CTA holds every routed id (its own
+    // warps just wrote them) — one warp builds the plan, no second handoff
+    trace_minmax(-1, 7);
+    if (warp == 0) plan_warp<true>(a.ids32, a.gw, T, a.K + a.S, E, bs, p, pad, lane, reinterpret_cast<int*>(xs));
+    trace_minmax(-1, 5);
+    return;
+  }
 
   // ---- last token tile overall: permute all T tokens ----
   __threadfence();

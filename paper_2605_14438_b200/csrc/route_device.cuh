@@ -496,4 +496,87 @@ __device__ __forceinline__ void plan_small_block(const int32_t* ids, const float
   }
 }
 
+// The plan of at most 32 (token, slot) entries by ONE warp (decode, T * Keff <=
+// 32): lane i holds entry i; same-expert lanes find each other with match_any
+// (a lane's rank among them = its position inside the expert's run, ascending
+// flat index), the experts' runs are ordered by expert id through a 32-entry
+// table in shared memory.  Same outputs as permute_block, no CTA barrier.
+// smem: 3 * 32 ints.
+template <bool CG>
+__device__ __forceinline__ void plan_warp(const int32_t* ids, const float* w, int T, int K, int E, int bs,
+                                          const PlanDev& p, bool pad, int lane, int* smem) {
+  int* le = smem;       // [32] leader experts (INT_MAX = none)
+  int* lp = smem + 32;  // [32] padded counts
+  int* lc = smem + 64;  // [32] counts
+  const int M = T * K;
+  int e = -1;
+  float wi = 0.0f;
+  if (lane < M) {
+    e = ld_maybe_cg<CG>(ids + lane);
+    if (w) wi = ld_maybe_cg<CG>(w + lane);
+  }
+  const bool valid = lane < M && e >= 0 && e < E;
+  const unsigned peers = __match_any_sync(0xffffffffu, valid ? e : E + lane);
+  const int within = __popc(peers & ((1u << lane) - 1u));
+  const int cnt = __popc(peers);
+  const bool leader = valid && within == 0;
+  const int padded = leader ? round_up(cnt, bs) : 0;
+  le[lane] = leader ? e : 0x7fffffff;
+  lp[lane] = padded;
+  lc[lane] = leader ? cnt : 0;
+  __syncwarp();
+  int before = 0, act_before = 0;
+#pragma unroll 8
+  for (int j = 0; j < 32; ++j) {
+    const int ej = le[j];
+    if (ej < e) {
+      before += lp[j];
+      ++act_before;
+    }
+  }
+  if (valid) {
+    const int pos = before + within;
+    const int t = lane / K;
+    p.tok[pos] = t;
+    p.slot[pos] = lane - t * K;
+    if (p.w) p.w[pos] = wi;
+    if (p.slot_pos) p.slot_pos[lane] = pos;
+    if (p.slot_expert) p.slot_expert[lane] = e;
+  } else if (lane < M) {
+    if (p.slot_pos) p.slot_pos[lane] = -1;
+    if (p.slot_expert) p.slot_expert[lane] = -1;
+  }
+  if (leader) {
+    p.active[act_before] = e;
+    if (pad)
+      for (int q = before + cnt; q < before + padded; ++q) {
+        p.tok[q] = -1;
+        p.slot[q] = -1;
+        if (p.w) p.w[q] = 0.0f;
+      }
+  }
+  const int n_act = __popc(__ballot_sync(0xffffffffu, leader));
+  const int n_real = __popc(__ballot_sync(0xffffffffu, valid));
+  const int n_pad = warp_sum_int(padded);
+  // counts / padded offsets of every expert (inactive: count 0)
+  for (int e2 = lane; e2 < E; e2 += 32) {
+    int off = 0, c = 0;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+      const int ej = le[j];
+      off += ej < e2 ? lp[j] : 0;
+      c += ej == e2 ? lc[j] : 0;
+    }
+    p.counts[e2] = c;
+    p.offsets[e2] = off;
+  }
+  if (lane == 0) {
+    p.offsets[E] = n_pad;
+    p.meta[0] = n_act;
+    p.meta[1] = n_pad;
+    p.meta[2] = n_real;
+    p.meta[3] = 0;
+  }
+}
+
 }  // namespace beam
