@@ -469,6 +469,33 @@ def run_ours(args):
                               "hbm_frac_of_measured": round(byt / sec / 1e9 / hbm_peak, 4)})
                 del p
 
+    # ---- mask-router training step: forward over all K candidates
+    #      + fused slot-dot / closed-form STE backward + x_n^T dA (cuBLAS) ---------
+    train = []
+    if not args.no_train:
+        for tt in (64, 8192):
+            p = run_point(B, w, tt, 0.5, 2, 1, flush, dev, seed=13)
+            x = p["h"].to(dev)
+            dy = torch.randn(tt, d, device=dev)
+            for _ in range(2):
+                B.mask_router_backward(x, blk, dy, beta=0.5)
+            evs = []
+            for _ in range(5):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                B.mask_router_backward(x, blk, dy, beta=0.5)
+                e1.record()
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+            us = float(np.mean([a.elapsed_time(b) for a, b in evs])) * 1e3
+            train.append({"T": tt, "s_target": 0.5, "us_per_step": round(us, 1),
+                          "inference_us_per_step": round(p["ms"] * 1e3, 1),
+                          "candidate_expert_flops": 6 * d * f * tt * k,
+                          "what": "beam.mask_router_backward: gate + every top-K candidate through the expert "
+                                  "kernels + fused slot-dot/STE + grad_weight GEMM (eager)"})
+            del p
+
     launches = lib.beam_kernel_launches() - launches0
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
@@ -499,6 +526,7 @@ def run_ours(args):
         "gpu_launches_per_step": launches_per_step,
         "gpu_launches_counted_total": int(launches),
         "sweep": sweep,
+        "train_mask_router": train,
     }
     print(json.dumps(line), flush=True)
 
@@ -516,6 +544,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--expert-path", default="auto", choices=("auto", "simt", "tc", "tc1", "stream"),
                     help="expert-stage kernels (diagnostics; default auto)")
     args = ap.parse_args()

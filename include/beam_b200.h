@@ -182,6 +182,34 @@ int beam_grouped_execute(const beam_layer_t* layer, const void* x, int x_dtype, 
 int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w, float* out,
                   beam_stream_t stream);
 
+/* ---- mask-router training ------------------------------------
+ * beam.ste_backward (beam.py:100-124), dense [T, N] f32:
+ *   grad = (upstream * weights + beta / (K*T) * [weights > 0]) * s * (1 - s),
+ *   s = sigmoid(pre_act) (tensor.py:406-411).  beta < 0 -> BEAM_ERR_ARG
+ *   (the reference's ContractError). */
+int beam_ste_backward(const float* upstream, const float* weights, const float* pre_act, int T,
+                      int N, int K, float beta, float* grad, beam_stream_t stream);
+/* beam.sparsity_loss (beam.py:87-97): sum over each token's top-K candidates
+ * of raw_mask, / (T*K).  raw_mask f32 [T, N], topk_ids int64 [T, K]; loss f32[1].
+ * Deterministic (one CTA, fixed summation order). */
+int beam_sparsity_loss(const float* raw_mask, const int64_t* topk_ids, int T, int N, int K,
+                       float* loss, beam_stream_t stream);
+/* Mask-router backward of beam_block_forward(training=True) (beam.py:146-157):
+ * the training forward evaluates EVERY top-K candidate (masked ones included,
+ * moe.py:223-279 compute_ids), so for L = sum(out * dy) + beta * sparsity_loss
+ *   dghat[t,k] = <dy[t], E_{topk[t,k]}(x_n[t])>            (dL_task/dghat)
+ *   grad_pre_act[t,i] = ste_backward(dghat scattered to [T,N], weights, a)
+ * One call: gate (fills outputs->topk_ids / weights / pre_activation [/ raw_mask],
+ * which must be non-NULL) -> plan over all candidates with unit weights ->
+ * experts -> fused slot-dot + closed-form STE kernel.  dy f32 [T, d_h];
+ * grad_pre_act f32 [T, N] (exact 0 off the candidate set); dghat f32 [T, K]
+ * and loss_reg f32[1] (= sparsity_loss, needs outputs->raw_mask) optional.
+ * Workspace: beam_workspace_bytes(layer, T, 0, block_size). */
+int beam_mask_backward(const beam_layer_t* layer, const void* h, int h_dtype, int T, const float* dy,
+                       float beta, int block_size, const beam_outputs_t* outputs, float* grad_pre_act,
+                       float* dghat, float* loss_reg, void* workspace, size_t workspace_bytes,
+                       beam_stream_t stream);
+
 /* Diagnostics.
  * beam_kernel_launches: kernels this library launched since load.
  * beam_profile_begin/end: record CUDA events on the launch stream at the stage

@@ -327,6 +327,67 @@ def beam_block_forward(h: np.ndarray, block: OracleBlock, block_size: int = 16) 
 
 
 # ---------------------------------------------------------------------------
+# mask-router training (beam.py:87-124, 146-157)
+# ---------------------------------------------------------------------------
+
+
+def sparsity_loss(raw_mask: np.ndarray, topk_indices: np.ndarray) -> float:
+    """beam.py:87-97: token-mean L1 of the raw mask over the top-K candidates."""
+    t, k = topk_indices.shape
+    sel = np.zeros(raw_mask.shape)
+    np.put_along_axis(sel, topk_indices, 1.0, axis=-1)
+    return float(np.sum(raw_mask * sel) / (t * k))
+
+
+def ste_backward(upstream: np.ndarray, weights: np.ndarray, pre_activation: np.ndarray,
+                 beta: float, k: int) -> np.ndarray:
+    """beam.py:100-124: (dL/dghat * g + beta/(K*T) * [g > 0]) * sigma'(a)."""
+    if beta < 0:
+        raise ContractError("beta must be non-negative")
+    t = upstream.shape[0]
+    indicator = (weights > 0.0).astype(np.float64)
+    s = sigmoid(pre_activation)
+    return (upstream * weights + (beta / (k * t)) * indicator) * (s * (1.0 - s))
+
+
+@dataclass
+class MaskGradResult:
+    out: np.ndarray            # training forward output (== inference, beam.py:146-157)
+    dghat: np.ndarray          # [T, K] dL_task/dghat at the candidate slots (rank order)
+    grad_pre_activation: np.ndarray  # [T, N]
+    grad_weight: np.ndarray    # [d, N] = x_n^T grad_pre_activation (mask_forward: a = x_n W_m)
+    loss_reg: float
+    decision: RouterDecision
+    mask: MaskDecision
+
+
+def mask_router_backward(h: np.ndarray, block: OracleBlock, dy: np.ndarray, beta: float) -> MaskGradResult:
+    """Mask-router gradient of L = sum(out * dy) + beta * sparsity_loss through
+    beam_block_forward(training=True) (beam.py:146-157): every top-K candidate is
+    evaluated (moe.py:223-279 compute_ids), dL_task/dghat_i = <dy, E_i(x_n)>,
+    then the closed form (beam.py:100-124)."""
+    x_n = block.normalize(h)
+    decision = topk_route(x_n, block.router_w, block.top_k)
+    maskdec = mask_forward(x_n, block.mask_w, block.tau)
+    t, k = decision.topk_indices.shape
+    ghat = decision.weights * maskdec.mask
+    y = np.zeros_like(x_n)
+    upstream = np.zeros_like(decision.weights)
+    dghat = np.zeros((t, k))
+    for row in range(t):
+        for r, e in sorted(enumerate(decision.topk_indices[row]), key=lambda p: p[1]):  # ascending expert
+            o = expert_forward(x_n[row : row + 1], *block.experts[e], block.activation)[0]
+            y[row] += ghat[row, e] * o
+            upstream[row, e] = float(dy[row] @ o)
+            dghat[row, r] = upstream[row, e]
+    for e in block.shared:
+        y = y + expert_forward(x_n, *e, block.activation)
+    grad = ste_backward(upstream, decision.weights, maskdec.pre_activation, beta, k)
+    return MaskGradResult(h + y, dghat, grad, x_n.T @ grad,
+                          sparsity_loss(maskdec.raw_mask, decision.topk_indices), decision, maskdec)
+
+
+# ---------------------------------------------------------------------------
 # routing strategies (baselines.py) — inference branch
 # ---------------------------------------------------------------------------
 

@@ -9,7 +9,18 @@ or a CUDA device every compute entry raises ``BeamNativeError``.
 
 from . import baselines, dispatch  # noqa: F401
 from ._lib import BeamNativeError  # noqa: F401
-from .beam import MaskDecision, MaskRouter, beam_block_forward, mask_forward, rms_norm, set_expert_path  # noqa: F401
+from .beam import (  # noqa: F401
+    MaskDecision,
+    MaskGrad,
+    MaskRouter,
+    beam_block_forward,
+    mask_forward,
+    mask_router_backward,
+    rms_norm,
+    set_expert_path,
+    sparsity_loss,
+    ste_backward,
+)
 from .moe import (  # noqa: F401
     Expert,
     MoEBlock,
@@ -23,5 +34,6 @@ from .tensor import ContractError, NumericError, ShapeError  # noqa: F401
 __all__ = [
     "BeamNativeError", "ContractError", "Expert", "MaskDecision", "MaskRouter", "MoEBlock",
     "MoEBlockConfig", "NumericError", "RouterDecision", "ShapeError", "beam_block_forward",
-    "baselines", "dispatch", "mask_forward", "rms_norm", "topk_route", "topk_select",
+    "baselines", "dispatch", "mask_forward", "mask_router_backward", "MaskGrad", "rms_norm",
+    "sparsity_loss", "ste_backward", "topk_route", "topk_select",
 ]

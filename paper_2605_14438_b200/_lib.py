@@ -36,6 +36,9 @@ EXPORTS = (
     "beam_group_by_expert",
     "beam_grouped_execute",
     "beam_rms_norm",
+    "beam_ste_backward",
+    "beam_sparsity_loss",
+    "beam_mask_backward",
     "beam_kernel_launches",
     "beam_set_expert_path",
     "beam_profile_begin",
@@ -125,6 +128,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_group_by_expert": (I, [P, I, I, I, I, P, P, P, P, P, P, P]),
         "beam_grouped_execute": (I, [LP, P, I, I, I, I, P, P, P, P, P, P, P, P, P, P, S, P]),
         "beam_rms_norm": (I, [P, I, I, I, P, P, P]),
+        "beam_ste_backward": (I, [P, P, P, I, I, I, ctypes.c_float, P, P]),
+        "beam_sparsity_loss": (I, [P, P, I, I, I, P, P]),
+        "beam_mask_backward": (I, [LP, P, I, I, P, ctypes.c_float, I, OP, P, P, P, P, S, P]),
         "beam_kernel_launches": (ctypes.c_ulonglong, []),
         "beam_set_expert_path": (I, [I]),
         "beam_profile_begin": (I, [I]),

@@ -219,6 +219,106 @@ def beam_block_forward(h, block: MoEBlock, training: bool = True, block_size: in
     return outs["out"], dec, md
 
 
+# ---------------------------------------------------------------------------
+# mask-router training (beam.py:87-124, 146-157)
+# ---------------------------------------------------------------------------
+
+
+def _f32(x, dev):
+    return as_torch(x).to(dev, torch.float32).contiguous()
+
+
+def sparsity_loss(raw_mask, topk_indices) -> torch.Tensor:
+    """beam.py:87-97: sum of raw_mask over each token's top-K candidates / (K*T)
+    (0-d fp32 tensor on the GPU; fixed-order fp64 accumulation)."""
+    raw = as_torch(raw_mask)
+    dev = raw.device if raw.is_cuda else _default_device()
+    raw = _f32(raw, dev)
+    ids = as_torch(topk_indices).to(dev, torch.int64).contiguous()
+    t, n = raw.shape
+    k = ids.shape[1]
+    out = torch.empty(1, dtype=torch.float32, device=dev)
+    _lib.check(_lib.load().beam_sparsity_loss(raw.data_ptr(), ids.data_ptr(), t, n, k, out.data_ptr(),
+                                              _runtime.stream_handle(dev)), "beam_sparsity_loss")
+    return out[0]
+
+
+def ste_backward(upstream, weights, decision: MaskDecision, beta: float, k: int) -> torch.Tensor:
+    """beam.py:100-124 closed form on the GPU:
+    dL/da = (upstream * g + beta/(K*T) * [g > 0]) * sigma'(a), [T, N] fp32."""
+    if beta < 0:
+        raise ContractError("beta must be non-negative")
+    a = as_torch(decision.pre_activation)
+    dev = a.device if a.is_cuda else _default_device()
+    a, up, w = _f32(a, dev), _f32(upstream, dev), _f32(weights, dev)
+    if up.shape != a.shape or w.shape != a.shape:
+        raise ShapeError("upstream, weights and pre_activation must all be [T, N]")
+    t, n = a.shape
+    grad = torch.empty_like(a)
+    _lib.check(_lib.load().beam_ste_backward(up.data_ptr(), w.data_ptr(), a.data_ptr(), t, n, int(k),
+                                             float(beta), grad.data_ptr(), _runtime.stream_handle(dev)),
+               "beam_ste_backward")
+    return grad
+
+
+@dataclass
+class MaskGrad:
+    """Mask-router gradient of one layer for L = sum(out * dy) + beta * sparsity_loss."""
+
+    grad_pre_activation: torch.Tensor  # [T, N] (exact 0 off each token's candidates)
+    grad_weight: torch.Tensor          # [d_h, N] = x_n^T grad_pre_activation
+    dghat: torch.Tensor                # [T, K] dL_task/dghat at the candidates (rank order)
+    loss_reg: torch.Tensor             # 0-d: sparsity_loss(raw_mask, topk_indices)
+    decision: RouterDecision
+    mask_decision: MaskDecision
+
+
+def mask_router_backward(h, block: MoEBlock, dy, beta: float = 0.0, block_size: int = 16) -> MaskGrad:
+    """Backward of beam_block_forward(training=True) (beam.py:146-157) to the mask
+    router, through the closed form ste_backward (beam.py:100-124): ONE C-ABI call
+    (beam_mask_backward) runs the gate, evaluates every top-K candidate on the
+    expert kernels (masked ones included) and fuses the slot dots with the STE
+    step; the [d_h, N] weight gradient x_n^T dA is a plain cuBLAS GEMM.  Expert
+    and router weights are frozen (BEAM trains the mask router only)."""
+    _check_block(block)
+    if beta < 0:
+        raise ContractError("beta must be non-negative")
+    if block_size < 1:
+        raise ContractError("block_size must be >= 1")
+    dev = block.device
+    x = as_torch(h)
+    if x.ndim != 2 or x.shape[1] != block.cfg.d_h:
+        raise ShapeError("h must be [tokens, d_h]")
+    if x.dtype not in (torch.float32, torch.bfloat16):
+        x = x.to(torch.float32)
+    x = x.to(dev).contiguous()
+    g = _f32(dy, dev)
+    if g.shape != x.shape:
+        raise ShapeError("dy must be [tokens, d_h]")
+    cfg = block.cfg
+    t, n, k = x.shape[0], cfg.num_experts, cfg.top_k
+    outs = LayerOutputs(t, cfg.d_h, n, k, x.dtype, dev)
+    grad = torch.empty(t, n, dtype=torch.float32, device=dev)
+    dghat = torch.empty(t, k, dtype=torch.float32, device=dev)
+    loss = torch.zeros(1, dtype=torch.float32, device=dev)
+    if t > 0:
+        desc = block.layer_desc(0.0)
+        lib = _lib.load()
+        ws = _runtime.workspace(lib.beam_workspace_bytes(ctypes.byref(desc), t, 0, block_size), dev)
+        o = outs.ctypes_outputs()
+        _lib.check(lib.beam_mask_backward(ctypes.byref(desc), x.data_ptr(),
+                                          _lib.BEAM_BF16 if x.dtype == torch.bfloat16 else _lib.BEAM_F32, t,
+                                          g.data_ptr(), float(beta), block_size, ctypes.byref(o),
+                                          grad.data_ptr(), dghat.data_ptr(), loss.data_ptr(), ws.data_ptr(),
+                                          ws.numel(), _runtime.stream_handle(dev)),
+                   "beam_mask_backward")
+    x_n = block.normalize(x) if block.norm_w is not None else x.float()
+    grad_w = x_n.t().matmul(grad)
+    dec = RouterDecision(logits=outs["logits"], topk_indices=outs["topk_ids"], weights=outs["weights"])
+    md = MaskDecision(pre_activation=outs["pre_activation"], raw_mask=outs["raw_mask"], mask=outs["mask"])
+    return MaskGrad(grad, grad_w, dghat, loss[0], dec, md)
+
+
 def set_expert_path(mode: str = "auto") -> None:
     """Choose the expert-stage kernels of beam_block_forward: "auto" (tcgen05
     grouped GEMM for prefill-sized batches, weight streaming for decode),

@@ -489,6 +489,65 @@ int beam_grouped_execute(const beam_layer_t* layer, const void* x, int x_dtype, 
   return BEAM_OK;
 }
 
+int beam_ste_backward(const float* upstream, const float* weights, const float* pre_act, int T, int N,
+                      int K, float beta, float* grad, beam_stream_t stream) {
+  if (!(beta >= 0.0f)) return BEAM_ERR_ARG;  // beam.py:117-118
+  if (T < 0 || N < 1 || K < 1) return BEAM_ERR_ARG;
+  if (T == 0) return BEAM_OK;
+  if (!upstream || !weights || !pre_act || !grad) return BEAM_ERR_ARG;
+  const float bt = (float)((double)beta / ((double)K * (double)T));
+  return status(launch_ste_dense(upstream, weights, pre_act, (long long)T * N, bt, grad,
+                                 reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int beam_sparsity_loss(const float* raw_mask, const int64_t* topk_ids, int T, int N, int K, float* loss,
+                       beam_stream_t stream) {
+  if (T < 0 || N < 1 || K < 0 || !loss) return BEAM_ERR_ARG;
+  if ((size_t)T * K > 0 && (!raw_mask || !topk_ids)) return BEAM_ERR_ARG;
+  return status(launch_sparsity_loss(raw_mask, topk_ids, T, N, K, loss, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int beam_mask_backward(const beam_layer_t* layer, const void* h, int h_dtype, int T, const float* dy,
+                       float beta, int block_size, const beam_outputs_t* o, float* grad, float* dghat,
+                       float* loss_reg, void* workspace, size_t workspace_bytes, beam_stream_t stream) {
+  int rc = validate(layer);
+  if (rc) return rc;
+  if (!(beta >= 0.0f) || T < 0 || block_size < 1 || !o) return BEAM_ERR_ARG;
+  if (h_dtype != BEAM_F32 && h_dtype != BEAM_BF16) return BEAM_ERR_ARG;
+  if (T > 0 && (!h || !dy || !grad || !o->topk_ids || !o->weights || !o->pre_activation)) return BEAM_ERR_ARG;
+  if (loss_reg && !o->raw_mask) return BEAM_ERR_ARG;
+  if (T == 0) return BEAM_OK;
+  const beam_layer_t& L = *layer;
+  const Dims g = dims_of(L);
+  Spec sp;
+  spec_of(L, nullptr, &sp);
+  LayerWs w;
+  if (carve(L, T, sp.Keff, block_size, workspace, &w, sp.cols) > workspace_bytes || !workspace)
+    return BEAM_ERR_WORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const void* X = nullptr;
+  BEAM_TRY(strided_input(g, h, h_dtype, T, w, &X, s));
+  // training forward, routing half (beam.py:141-142): decision + mask outputs
+  BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s, sp));
+  // every candidate, masked ones included (beam.py:146-157), with unit slot weights
+  BEAM_TRY(launch_candidates(o->topk_ids, T * g.K, w.ids32, w.gw, s));
+  BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, T, g.K, g.E, block_size, w.plan, w.pscratch, s));
+  const float* inv = L.has_norm ? w.inv : nullptr;
+  const float* nw = L.has_norm ? L.norm_w : nullptr;
+  if (w.tc) {
+    BEAM_TRY(launch_pack_x(X, h_dtype, inv, nw, g, w.plan, w.cap, w.xperm, s));
+    BEAM_TRY(launch_experts_tc(L, g, w.xperm, w.plan, w.cap, w.act16, w.opair, s));
+  } else {
+    BEAM_TRY(launch_gateup_simt(L, g, X, h_dtype, T, inv, nw, w.plan, w.act, s));
+    BEAM_TRY(launch_down_simt(L, g, T, w.plan, w.act, w.opair, s));
+  }
+  const float bt = (float)((double)beta / ((double)g.K * (double)T));
+  BEAM_TRY(launch_mask_grad(dy, g.d, w.opair, w.tc ? BEAM_BF16 : BEAM_F32, g.d_pad, w.plan.slot_pos,
+                            o->topk_ids, o->weights, o->pre_activation, T, g.N, g.K, bt, grad, dghat, s));
+  if (loss_reg) BEAM_TRY(launch_sparsity_loss(o->raw_mask, o->topk_ids, T, g.N, g.K, loss_reg, s));
+  return BEAM_OK;
+}
+
 int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w, float* out,
                   beam_stream_t stream) {
   if (T < 0 || d < 1) return BEAM_ERR_ARG;

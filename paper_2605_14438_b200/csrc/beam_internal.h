@@ -178,6 +178,17 @@ cudaError_t launch_combine(const PlanDev& p, const void* opair, int opair_dtype,
                            const void* h, int h_dtype, void* out, int out_dtype,
                            cudaStream_t s);
 
+// train.cu (mask-router backward)
+cudaError_t launch_candidates(const int64_t* topk, int M, int32_t* ids32, float* gw, cudaStream_t s);
+cudaError_t launch_mask_grad(const float* dy, int d, const void* O, int o_dtype, int d_pad,
+                             const int32_t* slot_pos, const int64_t* topk, const float* weights,
+                             const float* pre_act, int T, int N, int K, float bt, float* grad,
+                             float* dghat, cudaStream_t s);
+cudaError_t launch_ste_dense(const float* up, const float* w, const float* a, long long n, float bt,
+                             float* grad, cudaStream_t s);
+cudaError_t launch_sparsity_loss(const float* raw, const int64_t* topk, int T, int N, int K, float* loss,
+                                 cudaStream_t s);
+
 cudaError_t set_gate_trace(unsigned long long* buf);
 cudaError_t set_decode_trace(unsigned long long* buf);
 

@@ -79,3 +79,15 @@ def mask_margin_ok(ref, tol: float) -> np.ndarray:
     in both precisions; inclusive threshold) or farther than tol from it."""
     a = np.take_along_axis(ref.mask.pre_activation, ref.decision.topk_indices, 1)
     return np.all((np.abs(a) > tol) | (a == 0.0), axis=1)
+
+
+def ste_golden_block(g, i):
+    """Oracle block, h, dy, beta of golden mask-router gradient case i (tests/golden/ste.npz)."""
+    seed, d, f, n, k, sh, norm, t = (int(v) for v in g[f"c{i}_cfg"])
+    p = f"c{i}_"
+    experts = [(g[p + "w_gate"][e], g[p + "w_up"][e], g[p + "w_down"][e]) for e in range(n)]
+    shared = [(g[p + "s_gate"][s], g[p + "s_up"][s], g[p + "s_down"][s]) for s in range(sh)]
+    block = O.OracleBlock(d_h=d, d_ff=f, num_experts=n, top_k=k, router_w=g[p + "router_w"],
+                          experts=experts, shared=shared, norm_w=np.ones(d) if norm else None,
+                          mask_w=g[p + "mask_w"])
+    return block, g[p + "h"], g[p + "dy"], float(g[p + "beta"])

@@ -17,6 +17,10 @@ layer_*           — beam.beam_block_forward(training=False) (beam.py:127-165)
                     on small random blocks (norm / shared / non-zero mask router)
 strategies        — baselines.block_forward(training=False) (baselines.py:286-323) for every
                     routing strategy (top-k variants, moe_dynamic, ada_moe, beam, soft masks)
+ste               — mask-router gradient of beam_block_forward(training=True) through the
+                    reference's autograd tape (beam.py:87-157): L = sum(out * dy) + beta *
+                    sparsity_loss; pre-activation and mask-weight gradients (the closed form
+                    ste_backward, beam.py:100-124, is pinned to this tape by test_beam.py:231-242)
 q30route_dyadic   — Qwen3-30B-A3B router shape (N=128, K=8, d=2048), dyadic inputs,
                     so logits / pre-activations are exact in fp32 and fp64: top-K ids,
                     mask bits and the plan must match bit-for-bit.
@@ -114,7 +118,61 @@ def make_strategies():
     save("strategies", **arrays)
 
 
+def make_ste():
+    """Tape gradients of the BEAM training forward w.r.t. the mask router."""
+    ref.import_beamoe()
+    from beamoe.beam import MaskRouter, beam_block_forward, sparsity_loss
+    from beamoe.moe import MoEBlock, MoEBlockConfig
+    from beamoe.tensor import Tape, Tensor, add, mul, tsum
+
+    specs = [
+        # (seed, d, f, n, k, shared, has_norm, T, mask_std, beta)
+        (21, 32, 24, 8, 2, 0, True, 17, 1.0, 0.5),
+        (22, 16, 8, 4, 4, 0, False, 9, 0.8, 0.0),
+        (23, 32, 24, 16, 3, 1, True, 40, 2.0, 1.3),
+        (24, 24, 16, 6, 1, 0, True, 5, 0.5, 2.0),
+    ]
+    arrays = {}
+    for i, (seed, d, f, n, k, sh, norm, t, mstd, beta) in enumerate(specs):
+        rng = np.random.default_rng(seed)
+        cfg = MoEBlockConfig(d_h=d, d_ff=f, num_experts=n, top_k=k, num_shared=sh, has_norm=norm)
+        block = MoEBlock(cfg, rng, init_std=0.3)
+        block.mask_router = MaskRouter(Tensor(rng.normal(0, mstd, (d, n)), requires_grad=True))
+        h = rng.normal(size=(t, d))
+        dy = rng.normal(size=(t, d))
+        with Tape() as tape:
+            out, dec, mdec = beam_block_forward(Tensor(h), block, training=True)
+            task = tsum(mul(out, Tensor(dy)))
+            reg = sparsity_loss(mdec.raw_mask, dec.topk_indices)
+            tape.backward(add(task, mul(reg, beta)))
+        p = f"c{i}_"
+        arrays[p + "cfg"] = np.array([seed, d, f, n, k, sh, int(norm), t], np.int64)
+        arrays[p + "beta"] = np.float64(beta)
+        arrays[p + "h"] = h
+        arrays[p + "dy"] = dy
+        arrays[p + "router_w"] = block.router_w.data
+        arrays[p + "mask_w"] = block.mask_router.weight.data
+        arrays[p + "w_gate"] = np.stack([e.w_gate.data for e in block.experts])
+        arrays[p + "w_up"] = np.stack([e.w_up.data for e in block.experts])
+        arrays[p + "w_down"] = np.stack([e.w_down.data for e in block.experts])
+        if sh:
+            arrays[p + "s_gate"] = np.stack([e.w_gate.data for e in block.shared])
+            arrays[p + "s_up"] = np.stack([e.w_up.data for e in block.shared])
+            arrays[p + "s_down"] = np.stack([e.w_down.data for e in block.shared])
+        arrays[p + "out"] = out.data
+        arrays[p + "topk_ids"] = dec.topk_indices
+        arrays[p + "weights"] = dec.weights.data
+        arrays[p + "pre_activation"] = mdec.pre_activation.data
+        arrays[p + "raw_mask"] = mdec.raw_mask.data
+        arrays[p + "loss_reg"] = np.float64(reg.data)
+        arrays[p + "grad_pre_activation"] = mdec.pre_activation.grad
+        arrays[p + "grad_weight"] = block.mask_router.weight.grad
+    arrays["n_cases"] = np.int64(len(specs))
+    save("ste", **arrays)
+
+
 def main():
+    make_ste()
     make_strategies()
     beamoe = ref.import_beamoe()
     from beamoe import dispatch

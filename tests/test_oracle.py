@@ -145,3 +145,44 @@ def test_layer_matches_live_reference():
         r = O.beam_block_forward(h, ob)
         assert np.array_equal(out.data, r.out)
         assert np.array_equal(dec.topk_indices, r.decision.topk_indices)
+
+
+# ---------------------------------------------------------------------------
+# mask-router training (beam.py:87-157) against the reference's autograd tape
+# ---------------------------------------------------------------------------
+
+
+def test_mask_router_backward_matches_reference_tape(golden):
+    from _beamtest import ste_golden_block
+
+    g = golden("ste")
+    for i in range(int(g["n_cases"])):
+        block, h, dy, beta = ste_golden_block(g, i)
+        r = O.mask_router_backward(h, block, dy, beta)
+        p = f"c{i}_"
+        assert np.array_equal(r.decision.topk_indices, g[p + "topk_ids"])
+        # training forward == inference forward (test_beam.py:281-292 pins 1e-9)
+        assert np.max(np.abs(r.out - g[p + "out"])) < 1e-12
+        assert np.max(np.abs(r.grad_pre_activation - g[p + "grad_pre_activation"])) < 1e-10, i
+        assert np.max(np.abs(r.grad_weight - g[p + "grad_weight"])) < 1e-10, i
+        assert abs(r.loss_reg - float(g[p + "loss_reg"])) < 1e-14
+        # non-candidates receive exactly zero (test_beam.py:244-249)
+        off = np.ones_like(r.grad_pre_activation, dtype=bool)
+        np.put_along_axis(off, r.decision.topk_indices, False, -1)
+        assert np.all(g[p + "grad_pre_activation"][off] == 0.0)
+        assert np.all(r.grad_pre_activation[off] == 0.0)
+
+
+def test_ste_backward_kats():
+    """test_beam.py:251-257: zero upstream -> candidates strictly positive, rest 0;
+    beta < 0 is a ContractError (beam.py:117-118)."""
+    rng = np.random.default_rng(77)
+    t, n, k = 5, 6, 3
+    weights = np.zeros((t, n))
+    idx = np.stack([rng.choice(n, size=k, replace=False) for _ in range(t)])
+    np.put_along_axis(weights, idx, 1.0 / k, -1)
+    a = rng.normal(size=(t, n))
+    grad = O.ste_backward(np.zeros((t, n)), weights, a, beta=0.7, k=k)
+    assert np.all(grad[weights > 0] > 0.0) and np.all(grad[weights == 0] == 0.0)
+    with pytest.raises(O.ContractError):
+        O.ste_backward(np.zeros((t, n)), weights, a, beta=-1.0, k=k)
