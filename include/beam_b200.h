@@ -223,10 +223,11 @@ unsigned long long beam_kernel_launches(void);
 int beam_set_expert_path(int mode);
 int beam_profile_begin(int max_calls);
 int beam_profile_end(float* stage_ms, int* calls);
-/* Fused decode gate phase timestamps (%globaltimer ns) into a device buffer of 8
+/* Fused decode gate phase timestamps (%globaltimer ns) into a device buffer of 16
  * u64 (caller initialises [0],[2] to ~0 and the rest to 0); NULL disables:
  * {first CTA start, last CTA start, first / last projection done,
- *  last top-K tile done, permute done, last top-K tile start, permute start}. */
+ *  last top-K tile done, permute done, last top-K tile start, permute start,
+ *  token 0: partials summed, top-K selected, softmax done, outputs stored}. */
 int beam_trace_gate(unsigned long long* dev_buf);
 /* Phase timeline of the fused decode kernel: u64[64 + 12 * grid] (zeroed by the
  * caller); slot 64 + m * grid + cta = %globaltimer of CTA `cta` at mark m, slots

@@ -61,6 +61,13 @@ struct TopkArgs {
   int64_t* topk_ids;
   int64_t* masked_ids;
   float *logits, *weights, *pre_act, *raw_mask, *mask;  // dense [T, N] (optional)
+  // fused decode gate only: per-split partial sums of x^2 ([splits][T], from the
+  // projection CTAs, replaces the re-read of the token row for inv_rms), and a
+  // shared-memory mirror of ids32 / gw (entries t*(K+S)+k < 32) for the plan warp
+  const float* ss_part = nullptr;
+  int32_t* ids_s = nullptr;
+  float* gw_s = nullptr;
+  unsigned long long* trace = nullptr;  // diagnostics: %globaltimer at top-K sub-steps of token 0
 };
 
 int num_sms();

@@ -174,7 +174,7 @@ template <typename TX, int TT>
 __device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const float* __restrict__ nw,
                                                  const float* __restrict__ W, int T, int cols, int d,
                                                  int d_pad, int kr, float* __restrict__ P, float* xs,
-                                                 float* red_s) {
+                                                 float* red_s, float* __restrict__ ssp = nullptr) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int c0 = (blockIdx.x * 8 + wib) * kGemvCols;
   const int split = blockIdx.y;
@@ -201,6 +201,22 @@ __device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const
     }
   }
   __syncthreads();
+  if (ssp != nullptr && blockIdx.x == 0) {
+    // per-split partial sums of x^2 for inv_rms (the top-K step adds the splits
+    // in order instead of re-reading the token rows); overlaps the weight loads
+    for (int t = wib; t < nt; t += 8) {
+      float q = 0.0f;
+      for (int k4 = lane; k4 < (kn >> 2); k4 += 32) {
+        const float4 x = *reinterpret_cast<const float4*>(xs + t * kr + 4 * k4);
+        q = fmaf(x.x, x.x, q);
+        q = fmaf(x.y, x.y, q);
+        q = fmaf(x.z, x.z, q);
+        q = fmaf(x.w, x.w, q);
+      }
+      q = warp_sum(q);
+      if (lane == 0) ssp[(size_t)split * T + t0 + t] = q;
+    }
+  }
   float acc[kGemvCols * TT];
 #pragma unroll
   for (int i = 0; i < kGemvCols * TT; ++i) acc[i] = 0.0f;
@@ -348,11 +364,6 @@ constexpr int kFusedTT = 8;        // tokens per fused-gate tile (one warp per t
 // tile done, [7] permute start, [5] permute done.
 __device__ unsigned long long* g_gate_trace = nullptr;
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 __device__ __forceinline__ void trace_minmax(int lo, int hi) {
   unsigned long long* tr = g_gate_trace;
@@ -373,8 +384,9 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   __shared__ float red_s[8 * kGemvCols * kFusedTT];
   __shared__ int s_last;
   const int cols = a.cols;
+  float* ssp = nw != nullptr ? P + (size_t)kFusedMaxSplit * T * cols : nullptr;
   trace_minmax(0, 1);
-  router_gemv_body<TX, kFusedTT>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s);
+  router_gemv_body<TX, kFusedTT>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s, ssp);
   trace_minmax(2, 3);
 
   // ---- last CTA of this token tile: top-K + mask ----
@@ -388,16 +400,26 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   trace_minmax(-1, 6);
   const int t0 = tile * kFusedTT, nt = min(kFusedTT, T - t0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool one_warp_plan = gridDim.z == 1 && T * (a.K + a.S) <= 32;
+  TopkArgs b = a;
+  b.ss_part = ssp;
+  b.trace = g_gate_trace;
+  int* scratch = reinterpret_cast<int*>(xs);  // plan_warp: [0, 64 + E), E <= 256
+  if (one_warp_plan) {
+    b.ids_s = scratch + 320;
+    b.gw_s = reinterpret_cast<float*>(scratch + 352);
+  }
   for (int t = t0 + warp; t < t0 + nt; t += 8)
-    topk_token<TX, NPL, kFusedMaxSplit, true, KIND>(P, gridDim.y, T, X, t, lane, a);
+    topk_token<TX, NPL, kFusedMaxSplit, true, KIND>(P, gridDim.y, T, X, t, lane, b);
   if (threadIdx.x == 0) counters[tile] = 0;
   __syncthreads();
   trace_minmax(-1, 4);
-  if (gridDim.z == 1 && T * (a.K + a.S) <= 32) {
+  if (one_warp_plan) {
     // one token tile and <= 32 slots: this CTA holds every routed id (its own
-    // warps just wrote them) — one warp builds the plan, no second handoff
+    // warps just wrote them, mirrored in shared memory) — one warp builds the
+    // plan, no second handoff
     trace_minmax(-1, 7);
-    if (warp == 0) plan_warp<true>(a.ids32, a.gw, T, a.K + a.S, E, bs, p, pad, lane, reinterpret_cast<int*>(xs));
+    if (warp == 0) plan_warp<false>(b.ids_s, b.gw_s, T, a.K + a.S, E, bs, p, pad, lane, scratch);
     trace_minmax(-1, 5);
     return;
   }

@@ -41,6 +41,12 @@ __device__ __forceinline__ T ld_maybe_cg(const T* p) {
 }
 
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // One warp, one token.  L = projection partials [splits][T][a.cols]: router
 // logits in columns [0, Nr), mask pre-activations (if any) in [mask_off,
 // mask_off + N); X = the token rows (stride d_pad) for inv_rms.  NPL = ceil(Nr / 32).
@@ -61,7 +67,15 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
   const int N = a.N, Nr = KIND == BEAM_ROUTE_BEAM ? a.N : a.Nr, K = a.K, Keff = a.K + a.S;
   const int kind = KIND >= 0 ? KIND : a.kind;
   float inv = 1.0f;
-  if (a.has_norm) {  // tensor.py:485-487: (mean(x^2) + eps)^-1/2 over the real d entries
+  if (a.has_norm && a.ss_part != nullptr) {  // split partials from the projection CTAs
+    float ss = 0.0f;
+#pragma unroll
+    for (int sp = 0; sp < MAXSPLIT; ++sp) {
+      const float v = ld_maybe_cg<CG>(a.ss_part + (size_t)min(sp, splits - 1) * T + t);
+      ss += sp < splits ? v : 0.0f;
+    }
+    inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
+  } else if (a.has_norm) {  // tensor.py:485-487: (mean(x^2) + eps)^-1/2 over the real d entries
     const TX* row = X + (size_t)t * a.d_pad;
     float ss = 0.0f;
 #pragma unroll 8
@@ -123,6 +137,8 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
     v[i] *= inv;
     av[i] *= inv;
   }
+  const bool tr = a.trace != nullptr && t == 0 && lane == 0;
+  if (tr) a.trace[8] = gtimer();
 
   // Selection on 64-bit keys (order-preserving float bits << 32 | ~column): one
   // max per butterfly level, and the key order is exactly the reference's
@@ -154,6 +170,7 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
         key[i] = 0ull;
       }
   }
+  if (tr) a.trace[9] = gtimer();
   // the top logit (softmax shift) from the lane that holds column top_j
   float mine = 0.0f;
 #pragma unroll
@@ -169,6 +186,7 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
   for (int i = 0; i < NPL; ++i)
     if (dyn ? (lane + 32 * i < Nr) : (rank[i] >= 0)) part += expf(v[i] - top_val);
   const float denom = warp_sum(part);
+  if (tr) a.trace[10] = gtimer();
 
   // DYNAMIC: the kept prefix — count = #(cumulative mass < phi) + 1 over the
   // descending order (dynamic_select); ranks < K suffice unless the K most
@@ -244,6 +262,10 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
       const size_t o = (size_t)t * Keff + r;
       a.ids32[o] = keep ? j : -1;
       a.gw[o] = keep ? w : 0.0f;
+      if (a.ids_s != nullptr && o < 32) {
+        a.ids_s[o] = keep ? j : -1;
+        a.gw_s[o] = keep ? w : 0.0f;
+      }
       if (a.topk_ids) a.topk_ids[(size_t)t * K + r] = (kind == BEAM_ROUTE_ADA && j >= N) ? -1 : j;
       if (a.masked_ids) a.masked_ids[(size_t)t * K + r] = keep ? j : -1;
     }
@@ -259,11 +281,16 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
       }
     }
   }
+  if (tr) a.trace[11] = gtimer();
   // shared experts: always-on slots K..K+S-1, weight 1.0 (beam.py:163-164)
   for (int s = lane; s < a.S; s += 32) {
     const size_t o = (size_t)t * Keff + K + s;
     a.ids32[o] = N + s;
     a.gw[o] = 1.0f;
+    if (a.ids_s != nullptr && o < 32) {
+      a.ids_s[o] = N + s;
+      a.gw_s[o] = 1.0f;
+    }
   }
 }
 
@@ -500,14 +527,17 @@ __device__ __forceinline__ void plan_small_block(const int32_t* ids, const float
 // 32): lane i holds entry i; same-expert lanes find each other with match_any
 // (a lane's rank among them = its position inside the expert's run, ascending
 // flat index), the experts' runs are ordered by expert id through a 32-entry
-// table in shared memory.  Same outputs as permute_block, no CTA barrier.
-// smem: 3 * 32 ints.
+// table in shared memory; the offsets of all E experts come from one warp scan
+// over a padded-count table the leaders scatter into.  Same outputs as
+// permute_block, no CTA barrier.  ids / w may live in shared memory (the fused
+// gate hands them over from its top-K warps without an L2 round trip).
+// smem: 2 * 32 + E ints.
 template <bool CG>
 __device__ __forceinline__ void plan_warp(const int32_t* ids, const float* w, int T, int K, int E, int bs,
                                           const PlanDev& p, bool pad, int lane, int* smem) {
   int* le = smem;       // [32] leader experts (INT_MAX = none)
   int* lp = smem + 32;  // [32] padded counts
-  int* lc = smem + 64;  // [32] counts
+  int* tab = smem + 64; // [E] padded count per expert (0 = inactive)
   const int M = T * K;
   int e = -1;
   float wi = 0.0f;
@@ -515,6 +545,7 @@ __device__ __forceinline__ void plan_warp(const int32_t* ids, const float* w, in
     e = ld_maybe_cg<CG>(ids + lane);
     if (w) wi = ld_maybe_cg<CG>(w + lane);
   }
+  for (int e2 = lane; e2 < E; e2 += 32) tab[e2] = 0;
   const bool valid = lane < M && e >= 0 && e < E;
   const unsigned peers = __match_any_sync(0xffffffffu, valid ? e : E + lane);
   const int within = __popc(peers & ((1u << lane) - 1u));
@@ -523,8 +554,8 @@ __device__ __forceinline__ void plan_warp(const int32_t* ids, const float* w, in
   const int padded = leader ? round_up(cnt, bs) : 0;
   le[lane] = leader ? e : 0x7fffffff;
   lp[lane] = padded;
-  lc[lane] = leader ? cnt : 0;
   __syncwarp();
+  if (leader) tab[e] = padded;
   int before = 0, act_before = 0;
 #pragma unroll 8
   for (int j = 0; j < 32; ++j) {
@@ -557,19 +588,29 @@ __device__ __forceinline__ void plan_warp(const int32_t* ids, const float* w, in
   }
   const int n_act = __popc(__ballot_sync(0xffffffffu, leader));
   const int n_real = __popc(__ballot_sync(0xffffffffu, valid));
-  const int n_pad = warp_sum_int(padded);
-  // counts / padded offsets of every expert (inactive: count 0)
-  for (int e2 = lane; e2 < E; e2 += 32) {
-    int off = 0, c = 0;
-#pragma unroll 8
-    for (int j = 0; j < 32; ++j) {
-      const int ej = le[j];
-      off += ej < e2 ? lp[j] : 0;
-      c += ej == e2 ? lc[j] : 0;
-    }
-    p.counts[e2] = c;
-    p.offsets[e2] = off;
+  __syncwarp();
+  // counts / padded offsets of every expert (inactive: count 0): lane l owns the
+  // contiguous experts [l*per, (l+1)*per); exclusive warp scan of their sums
+  const int per = ceil_div(E, 32);
+  const int e0 = min(E, lane * per), e1 = min(E, e0 + per);
+  int run = 0;
+  for (int e2 = e0; e2 < e1; ++e2) run += tab[e2];
+  int incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
+  int off = incl - run;
+  for (int e2 = e0; e2 < e1; ++e2) {
+    const int pc = tab[e2];
+    p.offsets[e2] = off;
+    p.counts[e2] = 0;
+    off += pc;
+  }
+  const int n_pad = __shfl_sync(0xffffffffu, incl, 31);
+  __syncwarp();
+  if (leader) p.counts[e] = cnt;  // after the zero fill (same warp, ordered by __syncwarp)
   if (lane == 0) {
     p.offsets[E] = n_pad;
     p.meta[0] = n_act;

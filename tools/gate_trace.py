@@ -21,9 +21,10 @@ def main(flush_l2=True):
     blk = B.MoEBlock.from_weights(cfg, w["router"], (w["wg"], w["wu"], w["wd"]), norm_w=None,
                                   mask_w=w["mask"], dtype=torch.bfloat16, device=dev)
     lib = _lib.load()
-    tr = torch.zeros(8, dtype=torch.int64, device=dev)
+    tr = torch.zeros(16, dtype=torch.int64, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    names = ["start_skew", "proj_first", "proj_last", "topk_start", "topk_done", "permute_start", "permute_done"]
+    names = ["start_skew", "proj_first", "proj_last", "topk_start", "t0_loaded", "t0_selected", "t0_softmax",
+             "t0_stored", "topk_done", "permute_start", "permute_done"]
     for t in (1, 8, 64):
         hc = bench.make_tokens(t, 7)
         theta = bench.calibrate_theta(hc, w["router"], w["mask"], Q["k"], 0.5)
@@ -44,7 +45,8 @@ def main(flush_l2=True):
             lib.beam_trace_gate(None)
             v = tr.cpu().numpy().astype(np.float64)
             if it >= 2:
-                rows.append([v[1] - v[0], v[2] - v[0], v[3] - v[0], v[6] - v[0], v[4] - v[0], v[7] - v[0], v[5] - v[0]])
+                rows.append([v[1] - v[0], v[2] - v[0], v[3] - v[0], v[6] - v[0], v[8] - v[0], v[9] - v[0],
+                             v[10] - v[0], v[11] - v[0], v[4] - v[0], v[7] - v[0], v[5] - v[0]])
         med = np.median(np.array(rows), axis=0) / 1e3
         print(f"T={t} flush={flush_l2}: " + ", ".join(f"{n}={x:.2f}us" for n, x in zip(names, med)))
 
