@@ -282,6 +282,19 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------------------
 
 
+_CAPTURE_STREAMS = {}
+
+
+def _capture_stream(device):
+    """One capture stream per device for every graph the bench builds (so the
+    library's per-stream workspace is created once, outside any capture)."""
+    import torch
+
+    if device not in _CAPTURE_STREAMS:
+        _CAPTURE_STREAMS[device] = torch.cuda.Stream(device)
+    return _CAPTURE_STREAMS[device]
+
+
 class GpuLayer:
     """One BEAM block on the GPU plus preallocated outputs and a captured graph."""
 
@@ -296,8 +309,17 @@ class GpuLayer:
         self._fwd = layer_forward_into
         self.eager()
         torch.cuda.synchronize()
+        # warm up on the capture stream first: the library's workspace is cached
+        # per stream and zero-filled once on creation — created inside the capture,
+        # that fill would become part of every replay
+        cap = _capture_stream(x.device)
+        cap.wait_stream(torch.cuda.current_stream(x.device))
+        with torch.cuda.stream(cap):
+            self.eager()
+        torch.cuda.current_stream(x.device).wait_stream(cap)
+        torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        with torch.cuda.graph(self.graph, stream=cap):
             self.eager()
         torch.cuda.synchronize()
 

@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import threading
+import warnings
 
 import torch
 
@@ -23,6 +24,11 @@ def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
         buf = _workspaces.get(key)
         if buf is None or buf.numel() < nbytes:
             size = max(nbytes, int(buf.numel() * 1.5) if buf is not None else 0, 1 << 20)
+            if torch.cuda.is_current_stream_capturing():
+                warnings.warn("beam workspace created during CUDA-graph capture: its zero fill "
+                              "becomes part of every replay; run one call on the capture stream "
+                              "before capturing (torch.cuda.graph(..., stream=that_stream))",
+                              RuntimeWarning, stacklevel=3)
             # zero-filled once: the grid-completion counters at its start must
             # begin at 0 (the kernels reset them after every use)
             buf = torch.zeros(size, dtype=torch.uint8, device=device)

@@ -253,7 +253,7 @@ def bench_main(args, bench):
             torch.cuda.current_stream(dev).wait_stream(side)
             torch.cuda.synchronize()
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
+            with torch.cuda.graph(graph, stream=side):  # the warmed-up stream: no workspace fill captured
                 y_graph = layer.forward(x)
             torch.cuda.synchronize()
             graph.replay()
