@@ -113,6 +113,10 @@ typedef struct {
   float* raw_mask;         /* [T, N] sigmoid(a)    (MaskDecision.raw_mask)       */
   float* mask;             /* [T, N] 1.0 iff a >= threshold (MaskDecision.mask)  */
   int64_t* masked_ids;     /* [T, K] dispatch.mask_route output                  */
+  void* decision_event;    /* cudaEvent_t (may be NULL): beam_layer_forward[_routed]
+                              records it on the stream as soon as every decision
+                              output above is complete (after the gate), so a host
+                              caller can copy them out while the experts run      */
 } beam_outputs_t;
 
 /* Bytes of scratch the entries below need for T tokens, routed-id rows of width
@@ -210,6 +214,16 @@ int beam_mask_backward(const beam_layer_t* layer, const void* h, int h_dtype, in
                        float* dghat, float* loss_reg, void* workspace, size_t workspace_bytes,
                        beam_stream_t stream);
 
+/* Sparsity-trace rows of one layer call (analysis.SparsityTrace, analysis.py:15-86;
+ * trainer._record_routes, trainer.py:554-574), built on the device from the gate
+ * outputs: rows int64 [T*K][8] = {sequence_id, position, layer, rank (1-based),
+ * expert_id (= topk_ids), mask_bit (= masked_ids >= 0), phase (0 prefill, 1 decode),
+ * token_id}.  sequence_id / position / token_id int64 [T] may be NULL (0, t, 0).
+ * active_count (u64, may be NULL) is incremented by the executed slots (Avg-K). */
+int beam_trace_rows(const int64_t* topk_ids, const int64_t* masked_ids, const int64_t* sequence_id,
+                    const int64_t* position, const int64_t* token_id, int T, int K, int layer, int phase,
+                    int64_t* rows, unsigned long long* active_count, beam_stream_t stream);
+
 /* Diagnostics.
  * beam_kernel_launches: kernels this library launched since load.
  * beam_profile_begin/end: record CUDA events on the launch stream at the stage
@@ -235,6 +249,10 @@ int beam_trace_gate(unsigned long long* dev_buf);
 int beam_trace_decode(unsigned long long* dev_buf);
 const char* beam_last_cuda_error(void);
 const char* beam_build_info(void);
+/* 1 if `p` is page-locked host memory the GPU can address at the same pointer
+ * (UVA-mapped), so kernels may write results straight into it (the host-output
+ * path of beam_block_forward passes such a buffer as outputs->out). */
+int beam_host_mapped(const void* p);
 
 #ifdef __cplusplus
 }

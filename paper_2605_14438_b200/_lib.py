@@ -39,6 +39,7 @@ EXPORTS = (
     "beam_ste_backward",
     "beam_sparsity_loss",
     "beam_mask_backward",
+    "beam_trace_rows",
     "beam_kernel_launches",
     "beam_set_expert_path",
     "beam_profile_begin",
@@ -47,6 +48,7 @@ EXPORTS = (
     "beam_trace_decode",
     "beam_last_cuda_error",
     "beam_build_info",
+    "beam_host_mapped",
 )
 
 
@@ -100,6 +102,7 @@ class Outputs(ctypes.Structure):
         ("raw_mask", ctypes.c_void_p),
         ("mask", ctypes.c_void_p),
         ("masked_ids", ctypes.c_void_p),
+        ("decision_event", ctypes.c_void_p),
     ]
 
 
@@ -131,6 +134,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_ste_backward": (I, [P, P, P, I, I, I, ctypes.c_float, P, P]),
         "beam_sparsity_loss": (I, [P, P, I, I, I, P, P]),
         "beam_mask_backward": (I, [LP, P, I, I, P, ctypes.c_float, I, OP, P, P, P, P, S, P]),
+        "beam_trace_rows": (I, [P, P, P, P, P, I, I, I, I, P, P, P]),
         "beam_kernel_launches": (ctypes.c_ulonglong, []),
         "beam_set_expert_path": (I, [I]),
         "beam_profile_begin": (I, [I]),
@@ -139,6 +143,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_trace_decode": (I, [P]),
         "beam_last_cuda_error": (ctypes.c_char_p, []),
         "beam_build_info": (ctypes.c_char_p, []),
+        "beam_host_mapped": (I, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

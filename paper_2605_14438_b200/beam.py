@@ -19,6 +19,7 @@ from __future__ import annotations
 import ctypes
 import functools
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -99,61 +100,95 @@ def rms_norm(h, weight, eps: float = 1e-6) -> torch.Tensor:
 # ---------------------------------------------------------------------------
 
 
+_EXPERT_PATH = [0]  # beam_set_expert_path mode (changes the workspace layout)
+_F32_FIELDS = ("logits", "weights", "pre_activation", "raw_mask", "mask")
+_ID_FIELDS = ("topk_ids", "masked_ids")
+
+
 @functools.lru_cache(maxsize=256)
 def _outputs_layout(t: int, d: int, n: int, k: int, out_dtype: torch.dtype):
-    """(total bytes, ((name, byte offset, shape, dtype), ...)) of one layer's
-    outputs in a single flat buffer (256-byte aligned fields)."""
+    """Byte layout of one layer's outputs in a single flat buffer: the decision
+    outputs first (f32 [5, T, N] block, int64 [2, T, K] block), then `out`
+    [T, d] — so the decisions are one contiguous range a host caller can copy
+    while the experts still run.  Returns (total, f32_off, ids_off, out_off,
+    field byte offsets)."""
     es = torch.empty(0, dtype=out_dtype).element_size()
-    spec = [("out", (t, d), out_dtype, es), ("topk_ids", (t, k), torch.int64, 8),
-            ("masked_ids", (t, k), torch.int64, 8)]
-    spec += [(name, (t, n), torch.float32, 4)
-             for name in ("logits", "weights", "pre_activation", "raw_mask", "mask")]
-    fields, off = [], 0
-    for name, shape, dt, size in spec:
-        off = (off + 255) // 256 * 256
-        fields.append((name, off, shape, dt))
-        off += int(np.prod(shape)) * size
-    return off, tuple(fields)
+    f32_off = 0
+    ids_off = (f32_off + 5 * t * n * 4 + 255) // 256 * 256
+    out_off = (ids_off + 2 * t * k * 8 + 255) // 256 * 256
+    total = out_off + t * d * es
+    offs = {name: f32_off + i * t * n * 4 for i, name in enumerate(_F32_FIELDS)}
+    offs.update({name: ids_off + i * t * k * 8 for i, name in enumerate(_ID_FIELDS)})
+    offs["out"] = out_off
+    return total, f32_off, ids_off, out_off, tuple(offs.items())
 
 
 class LayerOutputs:
     """All outputs of one layer call carved from ONE flat buffer, so a host
-    caller pays a single device->host copy.  Views are created on first use
-    (a device-side staging copy never builds any)."""
+    caller pays one device->host copy for the decisions and one for `out`.
+    Views are built on first use, all at once (a device-side staging copy never
+    builds any)."""
 
     def __init__(self, t: int, d: int, n: int, k: int, out_dtype: torch.dtype, device, pin=False):
-        self.nbytes, self._fields = _outputs_layout(t, d, n, k, out_dtype)
+        self.shape = (t, d, n, k, out_dtype)
+        self.nbytes, self._f32_off, self._ids_off, self.out_off, self._offs = _outputs_layout(t, d, n, k, out_dtype)
         kw = dict(dtype=torch.uint8, device=device)
         self.buf = torch.empty(self.nbytes, pin_memory=pin, **kw) if pin else torch.empty(self.nbytes, **kw)
-        self._views = {}
+        self._views = None
+
+    def _build(self):
+        t, d, n, k, dt = self.shape
+        b = self.buf
+        f = b[self._f32_off : self._f32_off + 5 * t * n * 4].view(torch.float32).view(5, t, n).unbind(0)
+        ids = b[self._ids_off : self._ids_off + 2 * t * k * 8].view(torch.int64).view(2, t, k).unbind(0)
+        v = dict(zip(_F32_FIELDS, f))
+        v.update(zip(_ID_FIELDS, ids))
+        v["out"] = b[self.out_off :].view(dt).view(t, d)
+        self._views = v
+        return v
 
     def __getitem__(self, name):
-        v = self._views.get(name)
-        if v is None:
-            for fname, off, shape, dt in self._fields:
-                if fname == name:
-                    size = torch.empty(0, dtype=dt).element_size()
-                    n_el = int(np.prod(shape))
-                    v = self.buf[off : off + n_el * size].view(dt).view(shape)
-                    self._views[name] = v
-                    break
-            else:
-                raise KeyError(name)
-        return v
+        v = self._views if self._views is not None else self._build()
+        return v[name]
 
     @property
     def views(self):
-        return {fname: self[fname] for fname, _, _, _ in self._fields}
+        return dict(self._views if self._views is not None else self._build())
 
-    def ctypes_outputs(self) -> _lib.Outputs:
-        o = _lib.Outputs()
+    def ctypes_outputs(self, decision_event=None, out_ptr=None) -> _lib.Outputs:
         base = self.buf.data_ptr()
-        for name, off, _, _ in self._fields:
-            setattr(o, name, base + off)
+        o = _lib.Outputs(**{name: base + off for name, off in self._offs})
+        if decision_event is not None:
+            o.decision_event = decision_event
+        if out_ptr is not None:
+            o.out = out_ptr
         return o
 
     def copy_from(self, other: "LayerOutputs") -> None:
         self.buf.copy_(other.buf, non_blocking=True)
+
+    def copy_decisions_from(self, other: "LayerOutputs") -> None:
+        self.buf[: self.out_off].copy_(other.buf[: other.out_off], non_blocking=True)
+
+    def copy_out_from(self, other: "LayerOutputs") -> None:
+        self.buf[self.out_off :].copy_(other.buf[other.out_off :], non_blocking=True)
+
+
+_TLS = threading.local()
+
+
+def _copy_stream(dev: torch.device):
+    """(side stream, decision event) of a device for the host-output path (per
+    host thread)."""
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    per = getattr(_TLS, "copy", None)
+    if per is None:
+        per = _TLS.copy = {}
+    if key not in per:
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(dev))  # instantiates the CUDA event (lazy in torch)
+        per[key] = (torch.cuda.Stream(dev), ev)
+    return per[key]
 
 
 def _check_block(block: MoEBlock):
@@ -166,16 +201,31 @@ def _check_block(block: MoEBlock):
             "(dispatch/__init__.py:143-144)")
 
 
+_WS_CACHE: dict = {}
+
+
+def _ws_bytes(desc, t: int, block_size: int) -> int:
+    """beam_workspace_bytes, memoised on the values it depends on."""
+    key = (desc.d_h, desc.d_ff, desc.num_experts, desc.top_k, desc.num_shared, desc.wdtype, desc.has_norm,
+           desc.activation, t, block_size, _EXPERT_PATH[0])
+    v = _WS_CACHE.get(key)
+    if v is None:
+        v = _WS_CACHE[key] = _lib.load().beam_workspace_bytes(ctypes.byref(desc), t, 0, block_size)
+    return v
+
+
 def layer_forward_into(x: torch.Tensor, block: MoEBlock, outs: LayerOutputs,
-                       block_size: int = 16) -> None:
+                       block_size: int = 16, decision_event=None, out_ptr=None) -> None:
     """Launch the fused layer on ``x`` (device, [T, d], bf16/f32) writing into
-    preallocated ``outs`` — no allocation, no sync (CUDA-graph capturable)."""
+    preallocated ``outs`` — no allocation, no sync (CUDA-graph capturable).
+    ``decision_event`` (a torch.cuda.Event): recorded once the decision outputs
+    are complete; ``out_ptr``: write `out` there instead (e.g. mapped pinned
+    host memory)."""
     t = x.shape[0]
     desc = block.layer_desc(0.0)
     lib = _lib.load()
-    ws_bytes = lib.beam_workspace_bytes(ctypes.byref(desc), t, 0, block_size)
-    ws = _runtime.workspace(ws_bytes, x.device)
-    o = outs.ctypes_outputs()
+    ws = _runtime.workspace(_ws_bytes(desc, t, block_size), x.device)
+    o = outs.ctypes_outputs(decision_event.cuda_event if decision_event is not None else None, out_ptr)
     _lib.check(lib.beam_layer_forward(ctypes.byref(desc), x.data_ptr(),
                                       _lib.BEAM_BF16 if x.dtype == torch.bfloat16 else _lib.BEAM_F32,
                                       t, block_size, ctypes.byref(o), ws.data_ptr(), ws.numel(),
@@ -206,17 +256,40 @@ def beam_block_forward(h, block: MoEBlock, training: bool = True, block_size: in
     cfg = block.cfg
     t = xd.shape[0]
     outs = LayerOutputs(t, cfg.d_h, cfg.num_experts, cfg.top_k, xd.dtype, dev)
-    if t > 0:
-        layer_forward_into(xd, block, outs, block_size)
-    if host:
+    if host and t > 0:
+        # decisions leave the GPU on a side stream while the experts run; `out`
+        # follows the layer on the compute stream
+        side, ev = _copy_stream(dev)
+        main = torch.cuda.current_stream(dev)
         hb = LayerOutputs(t, cfg.d_h, cfg.num_experts, cfg.top_k, xd.dtype, "cpu",
                           pin=torch.cuda.is_available())
-        hb.copy_from(outs)
-        torch.cuda.current_stream(dev).synchronize()
-        outs = hb
-    dec = RouterDecision(logits=outs["logits"], topk_indices=outs["topk_ids"], weights=outs["weights"])
-    md = MaskDecision(pre_activation=outs["pre_activation"], raw_mask=outs["raw_mask"], mask=outs["mask"])
-    return outs["out"], dec, md
+        # `out` is written by the combine kernel straight into the (UVA-mapped)
+        # pinned host buffer: no trailing device->host copy
+        host_out = hb.buf.data_ptr() + hb.out_off
+        direct = _lib.load().beam_host_mapped(host_out) == 1
+        layer_forward_into(xd, block, outs, block_size, decision_event=ev, out_ptr=host_out if direct else None)
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            hb.copy_decisions_from(outs)
+        if not direct:
+            hb.copy_out_from(outs)
+        # result views are host-side bookkeeping: built while the GPU still works
+        res = _results(hb)
+        side.synchronize()
+        main.synchronize()
+        return res
+    elif t > 0:
+        layer_forward_into(xd, block, outs, block_size)
+    elif host:
+        outs = LayerOutputs(t, cfg.d_h, cfg.num_experts, cfg.top_k, xd.dtype, "cpu")
+    return _results(outs)
+
+
+def _results(outs: LayerOutputs):
+    v = outs.views
+    dec = RouterDecision(logits=v["logits"], topk_indices=v["topk_ids"], weights=v["weights"])
+    md = MaskDecision(pre_activation=v["pre_activation"], raw_mask=v["raw_mask"], mask=v["mask"])
+    return v["out"], dec, md
 
 
 # ---------------------------------------------------------------------------
@@ -326,3 +399,4 @@ def set_expert_path(mode: str = "auto") -> None:
     CTA pairs) or "tc1" (tcgen05 always, 1-SM kernel)."""
     code = {"auto": 0, "simt": 1, "tc": 2, "tc1": 3, "stream": 4}[mode]
     _lib.check(_lib.load().beam_set_expert_path(code), "beam_set_expert_path")
+    _EXPERT_PATH[0] = code

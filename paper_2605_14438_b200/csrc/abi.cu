@@ -327,6 +327,7 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
     // decode: the whole layer in one persistent kernel
     BEAM_TRY(launch_decode_fused(L, g, X, h_dtype, T, topk_args(L, g, o, w, sp), w.logits2, w.act,
                                  reinterpret_cast<unsigned*>(w.counters + 32), o->out, s));
+    if (o->decision_event) BEAM_TRY(cudaEventRecord(static_cast<cudaEvent_t>(o->decision_event), s));
     for (int m = 1; m < kStageMarks; ++m) prof_mark(m, s);
     return BEAM_OK;
   }
@@ -340,6 +341,7 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
     prof_mark(1, s);
     BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, T, sp.Keff, g.E, block_size, w.plan, w.pscratch, s));
   }
+  if (o->decision_event) BEAM_TRY(cudaEventRecord(static_cast<cudaEvent_t>(o->decision_event), s));
   prof_mark(2, s);
   if (w.tc) {
     BEAM_TRY(launch_pack_x(X, h_dtype, L.has_norm ? w.inv : nullptr, L.has_norm ? L.norm_w : nullptr, g,
@@ -548,6 +550,15 @@ int beam_mask_backward(const beam_layer_t* layer, const void* h, int h_dtype, in
   return BEAM_OK;
 }
 
+int beam_trace_rows(const int64_t* topk_ids, const int64_t* masked_ids, const int64_t* sequence_id,
+                    const int64_t* position, const int64_t* token_id, int T, int K, int layer, int phase,
+                    int64_t* rows, unsigned long long* active_count, beam_stream_t stream) {
+  if (T < 0 || K < 1 || (phase != 0 && phase != 1)) return BEAM_ERR_ARG;
+  if (T > 0 && (!topk_ids || !masked_ids || !rows)) return BEAM_ERR_ARG;
+  return status(launch_trace_rows(topk_ids, masked_ids, sequence_id, position, token_id, T, K, layer, phase, rows,
+                                  active_count, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w, float* out,
                   beam_stream_t stream) {
   if (T < 0 || d < 1) return BEAM_ERR_ARG;
@@ -603,6 +614,15 @@ int beam_trace_gate(unsigned long long* dev_buf) { return status(beam::set_gate_
 int beam_trace_decode(unsigned long long* dev_buf) { return status(beam::set_decode_trace(dev_buf)); }
 
 const char* beam_last_cuda_error(void) { return g_last_error; }
+
+int beam_host_mapped(const void* p) {
+  cudaPointerAttributes a;
+  if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer == p ? 1 : 0;
+}
 
 #define BEAM_STR2(x) #x
 #define BEAM_STR(x) BEAM_STR2(x)

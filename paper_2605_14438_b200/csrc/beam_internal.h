@@ -196,6 +196,11 @@ cudaError_t launch_ste_dense(const float* up, const float* w, const float* a, lo
 cudaError_t launch_sparsity_loss(const float* raw, const int64_t* topk, int T, int N, int K, float* loss,
                                  cudaStream_t s);
 
+// trace.cu (SparsityTrace rows from the gate outputs)
+cudaError_t launch_trace_rows(const int64_t* topk, const int64_t* masked, const int64_t* seq,
+                              const int64_t* pos, const int64_t* tok, int T, int K, int layer, int phase,
+                              int64_t* rows, unsigned long long* active, cudaStream_t s);
+
 cudaError_t set_gate_trace(unsigned long long* buf);
 cudaError_t set_decode_trace(unsigned long long* buf);
 

@@ -21,6 +21,9 @@ ste               — mask-router gradient of beam_block_forward(training=True) 
                     reference's autograd tape (beam.py:87-157): L = sum(out * dy) + beta *
                     sparsity_loss; pre-activation and mask-weight gradients (the closed form
                     ste_backward, beam.py:100-124, is pinned to this tape by test_beam.py:231-242)
+trace             — analysis.SparsityTrace (analysis.py:19-112) CSV text and the Avg-K
+                    reductions (avg_k every group key, position_mask_prob, expert_load)
+                    over seeded routing cells in both phases
 q30route_dyadic   — Qwen3-30B-A3B router shape (N=128, K=8, d=2048), dyadic inputs,
                     so logits / pre-activations are exact in fp32 and fp64: top-K ids,
                     mask bits and the plan must match bit-for-bit.
@@ -171,7 +174,51 @@ def make_ste():
     save("ste", **arrays)
 
 
+def make_trace():
+    """SparsityTrace rows / CSV / Avg-K metrics from the reference."""
+    import tempfile
+
+    ref.import_beamoe()
+    from beamoe import analysis
+
+    rng = np.random.default_rng(6000)
+    tr = analysis.SparsityTrace()
+    arrays = {}
+    calls = []
+    for layer in range(3):
+        for phase, seq in (("prefill", 0), ("decode", 1)):
+            t, n, k = 9, 16, 4
+            ids = np.stack([rng.choice(n, size=k, replace=False) for _ in range(t)]).astype(np.int64)
+            ids[rng.random((t, k)) < 0.05] = -1          # null slots (ada_moe)
+            bits = (rng.random((t, k)) < 0.6).astype(np.int64)
+            bits[ids < 0] = 0
+            masked = np.where(bits == 1, ids, -1)
+            pos = rng.permutation(40)[:t].astype(np.int64)
+            tok = rng.integers(0, 50, t).astype(np.int64)
+            for i in range(t):
+                tr.record_cell(seq, int(pos[i]), layer, ids[i], bits[i], phase, int(tok[i]))
+            calls.append((ids, masked, pos, tok, layer, phase, seq))
+    for c, (ids, masked, pos, tok, layer, phase, seq) in enumerate(calls):
+        arrays[f"ids_{c}"], arrays[f"masked_{c}"], arrays[f"pos_{c}"], arrays[f"tok_{c}"] = ids, masked, pos, tok
+        arrays[f"meta_{c}"] = np.array([layer, analysis.PHASES.index(phase), seq], np.int64)
+    arrays["n_calls"] = np.int64(len(calls))
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "t.csv")
+        tr.to_csv(path)
+        arrays["csv"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    import json
+
+    metrics = {g: {repr(k2): v for k2, v in analysis.avg_k(tr, g).items()} for g in analysis.GROUP_KEYS}
+    metrics["position_mask_prob"] = {repr(k2): v for k2, v in analysis.position_mask_prob(tr).items()}
+    before, after = analysis.expert_load(tr)
+    metrics["expert_load_routed"] = {repr(k2): v for k2, v in before.items()}
+    metrics["expert_load_kept"] = {repr(k2): v for k2, v in after.items()}
+    arrays["metrics_json"] = np.frombuffer(json.dumps(metrics, sort_keys=True).encode(), dtype=np.uint8)
+    save("trace", **arrays)
+
+
 def main():
+    make_trace()
     make_ste()
     make_strategies()
     beamoe = ref.import_beamoe()

@@ -61,7 +61,7 @@ def test_struct_layout_matches_header(lib_path):
 
     # 9 x 4-byte fields (8 int + 1 float), then 4 pointers
     assert ctypes.sizeof(_lib.LayerDesc) == 9 * 4 + 4 + 4 * 8
-    assert ctypes.sizeof(_lib.Outputs) == 8 * 8
+    assert ctypes.sizeof(_lib.Outputs) == 9 * 8  # 8 output pointers + decision_event
 
 
 def test_workspace_query_is_cpu_only(lib_path):
