@@ -7,7 +7,7 @@ C ABI in ``include/beam_b200.h``.  No CPU fallback: without the built library
 or a CUDA device every compute entry raises ``BeamNativeError``.
 """
 
-from . import baselines, dispatch  # noqa: F401
+from . import analysis, baselines, dispatch, lm  # noqa: F401
 from ._lib import BeamNativeError  # noqa: F401
 from .beam import (  # noqa: F401
     MaskDecision,

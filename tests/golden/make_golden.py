@@ -24,6 +24,9 @@ ste               — mask-router gradient of beam_block_forward(training=True) 
 trace             — analysis.SparsityTrace (analysis.py:19-112) CSV text and the Avg-K
                     reductions (avg_k every group key, position_mask_prob, expert_load)
                     over seeded routing cells in both phases
+lm                — trainer.TinyMoELM (trainer.py:150-257) with BEAM routing and seeded mask
+                    routers: forward logits, sample_greedy tokens across the sliding window
+                    (trainer.py:638-673) with its SparsityTrace CSV, evaluate() (:577-636)
 q30route_dyadic   — Qwen3-30B-A3B router shape (N=128, K=8, d=2048), dyadic inputs,
                     so logits / pre-activations are exact in fp32 and fp64: top-K ids,
                     mask bits and the plan must match bit-for-bit.
@@ -217,7 +220,47 @@ def make_trace():
     save("trace", **arrays)
 
 
+LM_CFG = dict(vocab_size=40, d_h=32, n_layers=2, n_heads=4, context_length=12, d_ff=48, num_experts=8,
+              top_k=4, seed=5)
+
+
+def lm_mask_weights(d, n, layers):
+    rng = np.random.default_rng(77)
+    return [rng.normal(0.0, 0.5, (d, n)) for _ in range(layers)]
+
+
+def make_lm():
+    """Reference TinyMoELM (BEAM strategy, seeded mask routers) outputs."""
+    import tempfile
+
+    ref.import_beamoe()
+    from beamoe import analysis
+    from beamoe.baselines import RoutingStrategy
+    from beamoe.trainer import ModelConfig, TinyMoELM, evaluate, sample_greedy
+
+    cfg = ModelConfig(strategy=RoutingStrategy("beam"), **LM_CFG)
+    model = TinyMoELM(cfg)
+    for layer, w in zip(model.layers, lm_mask_weights(cfg.d_h, cfg.num_experts, cfg.n_layers)):
+        layer["block"].mask_router.weight.data[...] = w
+    rng = np.random.default_rng(8)
+    ids = rng.integers(0, cfg.vocab_size, (2, cfg.context_length))
+    logits, routes = model.forward(ids, training=False)
+    prompt = rng.integers(0, cfg.vocab_size, 5)
+    trace = analysis.SparsityTrace()
+    gen = sample_greedy(model, prompt, 14, trace=trace, sequence_id=3)
+    corpus = rng.integers(0, cfg.vocab_size, 101)
+    ev = evaluate(model, corpus, batch_size=3)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "t.csv")
+        trace.to_csv(path)
+        csv_bytes = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    save("lm", ids=ids, logits=logits.data, kept_0=routes[0].kept_ids, kept_1=routes[1].kept_ids,
+         prompt=prompt, generated=gen, corpus=corpus, perplexity=np.float64(ev.perplexity),
+         avg_k=np.float64(ev.avg_k), token_count=np.int64(ev.token_count), trace_csv=csv_bytes)
+
+
 def main():
+    make_lm()
     make_trace()
     make_ste()
     make_strategies()

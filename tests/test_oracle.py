@@ -186,3 +186,30 @@ def test_ste_backward_kats():
     assert np.all(grad[weights > 0] > 0.0) and np.all(grad[weights == 0] == 0.0)
     with pytest.raises(O.ContractError):
         O.ste_backward(np.zeros((t, n)), weights, a, beta=-1.0, k=k)
+
+
+def test_lm_init_matches_reference_draws():
+    """paper_2605_14438_b200.lm.TinyMoELM draws its parameters like
+    trainer.TinyMoELM (trainer.py:153-176): same seed -> same weights."""
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    ref.import_beamoe()
+    import torch
+    from beamoe.baselines import RoutingStrategy as RS
+    from beamoe.trainer import ModelConfig as MC, TinyMoELM as TM
+
+    from paper_2605_14438_b200 import lm
+    from paper_2605_14438_b200.baselines import RoutingStrategy
+
+    kw = dict(vocab_size=40, d_h=32, n_layers=2, n_heads=4, context_length=12, d_ff=48, num_experts=8,
+              top_k=4, seed=5)
+    r = TM(MC(strategy=RS("beam"), **kw))
+    m = lm.TinyMoELM(lm.ModelConfig(strategy=RoutingStrategy("beam"), **kw), device="cpu")
+    f32 = lambda a: np.asarray(a, np.float32)  # noqa: E731
+    assert np.array_equal(m.wte.numpy(), f32(r.wte.data))
+    assert np.array_equal(m.lm_head.numpy(), f32(r.lm_head.data))
+    for a, b in zip(m.layers, r.layers):
+        for w in ("wq", "wk", "wv", "wo"):
+            assert np.array_equal(a[w].numpy(), f32(b[w].data))
+        assert np.array_equal(a["block"].router_w.numpy(), f32(b["block"].router_w.data))
+    del torch
