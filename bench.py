@@ -378,6 +378,51 @@ def run_point(B, w, t, s, steps, warmup, flush, dev, seed=7, block_size=16):
     return dict(layer=layer, theta=theta, h=h, ms=float(np.mean(ms)), r=r, e_act=e_act, s_real=s_real)
 
 
+def run_lm_decode(args, new_tokens: int = 48):
+    """trainer.sample_greedy on the GPU (KV cache, eager vs one CUDA graph per
+    step) next to the reference's own sample_greedy on the host, same seed /
+    BEAM strategy / prompt; ms per generated token (the window never slides)."""
+    import torch
+
+    from paper_2605_14438_b200 import lm as L
+    from paper_2605_14438_b200.baselines import RoutingStrategy
+
+    kw = dict(vocab_size=256, d_h=64, n_layers=2, n_heads=4, context_length=64, d_ff=128, num_experts=8,
+              top_k=4, seed=0)
+    m = L.TinyMoELM(L.ModelConfig(strategy=RoutingStrategy("beam"), **kw))
+    rng = np.random.default_rng(77)
+    masks = [rng.normal(0.0, 0.5, (kw["d_h"], kw["num_experts"])) for _ in range(kw["n_layers"])]
+    for layer, w in zip(m.layers, masks):
+        layer["block"].mask_router.weight.copy_(torch.from_numpy(w))
+    prompt = np.random.default_rng(3).integers(0, kw["vocab_size"], 8)
+    res = {"config": {**kw, "strategy": "beam", "prompt": 8, "new_tokens": new_tokens}}
+    for g in (False, True):
+        L.sample_greedy(m, prompt, 4, use_graph=g)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gen = L.sample_greedy(m, prompt, new_tokens, use_graph=g)
+        res["ms_per_token_graph" if g else "ms_per_token_eager"] = round((time.perf_counter() - t0) * 1e3 / new_tokens, 3)
+    if not args.no_cpu:
+        try:
+            from oracle import ref
+
+            ref.import_beamoe()
+            from beamoe.baselines import RoutingStrategy as RS
+            from beamoe.trainer import ModelConfig as MC, TinyMoELM as TM, sample_greedy as sg
+
+            rm = TM(MC(strategy=RS("beam"), **kw))
+            for layer, w in zip(rm.layers, masks):
+                layer["block"].mask_router.weight.data[...] = w
+            t0 = time.perf_counter()
+            rgen = sg(rm, prompt, 16)
+            res["reference_ms_per_token"] = round((time.perf_counter() - t0) * 1e3 / 16, 3)
+            res["tokens_match_reference"] = bool(np.array_equal(rgen, gen[:16]))
+        except Exception as e:  # reference package not built on this box
+            res["reference_ms_per_token"] = None
+            res["reference_error"] = str(e)[:120]
+    return res
+
+
 def run_ours(args):
     import torch
 
@@ -518,6 +563,11 @@ def run_ours(args):
                                   "kernels + fused slot-dot/STE + grad_weight GEMM (eager)"})
             del p
 
+    # ---- tiny MoE LM greedy decoding: ms per generated token ------
+    lm_line = None
+    if not args.no_train:
+        lm_line = run_lm_decode(args)
+
     launches = lib.beam_kernel_launches() - launches0
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
@@ -549,6 +599,7 @@ def run_ours(args):
         "gpu_launches_counted_total": int(launches),
         "sweep": sweep,
         "train_mask_router": train,
+        "lm_greedy_decode": lm_line,
     }
     print(json.dumps(line), flush=True)
 

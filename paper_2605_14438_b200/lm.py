@@ -89,7 +89,6 @@ class TinyMoELM:
             self.layers.append(layer)
         self.final_norm = torch.ones(d, device=self.device)
         self.lm_head = p((d, cfg.vocab_size))
-        self._graph = None
 
     # -- full forward (trainer.py:217-250, training=False) -------------------------
     def _heads(self, z, b, t):
@@ -134,6 +133,18 @@ class TinyMoELM:
         return x @ self.lm_head, routes
 
     # -- cached decode step ----------------------------------------------------------
+    def _decode_state(self, binarize_soft: bool):
+        """KV cache, step inputs and the captured step graph of batch-1 decoding
+        (kept on the model so the graph is captured once)."""
+        st = getattr(self, "_dstate", {}).get(binarize_soft)
+        if st is None:
+            st = {"kv": self._kv_cache(1), "tok": torch.zeros(1, dtype=torch.int64, device=self.device),
+                  "pos": torch.zeros((), dtype=torch.int64, device=self.device), "graph": None, "out": None}
+            if not hasattr(self, "_dstate"):
+                self._dstate = {}
+            self._dstate[binarize_soft] = st
+        return st
+
     def _kv_cache(self, b):
         cfg = self.cfg
         hd = cfg.d_h // cfg.n_heads
@@ -175,7 +186,8 @@ def sample_greedy(model: TinyMoELM, prompt_ids, max_new_tokens: int, trace=None,
     generated cells as decode (``analysis.SparsityTrace``)."""
     cfg = model.cfg
     ids = list(np.asarray(prompt_ids, dtype=np.int64)[-cfg.context_length:])
-    kv = model._kv_cache(1)
+    st = model._decode_state(binarize_soft)  # persistent cache / step tensors / graph
+    kv, tok, pos = st["kv"], st["tok"], st["pos"]
     window = np.asarray(ids, dtype=np.int64)[None, :]
     logits, routes = model.forward(window, binarize_soft=binarize_soft, _kv=kv)
     if trace is not None:
@@ -183,9 +195,6 @@ def sample_greedy(model: TinyMoELM, prompt_ids, max_new_tokens: int, trace=None,
     last = logits[0, -1]
     generated = []
     abs_pos = len(ids)
-    tok = torch.zeros(1, dtype=torch.int64, device=model.device)
-    pos = torch.zeros((), dtype=torch.int64, device=model.device)
-    graph, g_out = None, None
     for _ in range(max_new_tokens):
         nxt = int(torch.argmax(last))
         generated.append(nxt)
@@ -201,10 +210,10 @@ def sample_greedy(model: TinyMoELM, prompt_ids, max_new_tokens: int, trace=None,
             tok.fill_(nxt)
             pos.fill_(len(ids) - 1)
             if use_graph:
-                if graph is None:
-                    graph, g_out = _capture_step(model, tok, pos, kv, binarize_soft)
-                graph.replay()
-                step_logits, rr_cells = g_out
+                if st["graph"] is None:
+                    st["graph"], st["out"] = _capture_step(model, tok, pos, kv, binarize_soft)
+                st["graph"].replay()
+                step_logits, rr_cells = st["out"]
             else:
                 step_logits, rr_cells = model._decode_step(tok, pos, kv, binarize_soft)
             last = step_logits[0]
