@@ -99,6 +99,20 @@ __device__ __forceinline__ int warp_sum_int(int v) {
   return v;
 }
 
+// Two fp32 FMAs in one Blackwell FFMA2 (fma.rn.f32x2): (a0, a1) += (w0, w1) * (x, x).
+// Same per-lane rounding as two fmaf calls; the operand pairs are register pairs
+// ptxas allocates adjacently (no extra moves in the loops that use it).
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float w0, float w1, float x) {
+  asm("{\n\t.reg .b64 ra, rw, rx;\n\t"
+      "mov.b64 ra, {%0, %1};\n\t"
+      "mov.b64 rw, {%2, %3};\n\t"
+      "mov.b64 rx, {%4, %4};\n\t"
+      "fma.rn.f32x2 ra, rw, rx, ra;\n\t"
+      "mov.b64 {%0, %1}, ra;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(w0), "f"(w1), "f"(x));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

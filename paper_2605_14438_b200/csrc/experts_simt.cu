@@ -280,14 +280,17 @@ __device__ __forceinline__ void gateup_warp_tile(const TW* __restrict__ W, int r
         for (int j = 0; j < TB; ++j) xf[j][e] *= ge;
       }
     }
+    // rows in pairs (2p, 2p+1) through FFMA2: half the FMA instructions
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float wf[EPC];
-      unpack<TW>(wv[q], wf);
+    for (int p2 = 0; p2 < 4; ++p2) {
+      float wa[EPC], wb[EPC];
+      unpack<TW>(wv[2 * p2], wa);
+      unpack<TW>(wv[2 * p2 + 1], wb);
 #pragma unroll
       for (int j = 0; j < TB; ++j)
 #pragma unroll
-        for (int e = 0; e < EPC; ++e) acc[q * TB + j] = fmaf(wf[e], xf[j][e], acc[q * TB + j]);
+        for (int e = 0; e < EPC; ++e)
+          ffma2(acc[(2 * p2) * TB + j], acc[(2 * p2 + 1) * TB + j], wa[e], wb[e], xf[j][e]);
     }
   }
   warp_reduce_to_smem<8 * TB>(acc, red, lane);
