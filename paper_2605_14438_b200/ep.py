@@ -213,6 +213,9 @@ def bench_main(args, bench):
 
     import paper_2605_14438_b200 as B
 
+    # a single process without torchrun (BEAM_BENCH_FORCE_EP=1 check): rank 0 of 1
+    for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29511")):
+        os.environ.setdefault(k, v)
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
