@@ -51,32 +51,35 @@ SWEEP_S = (0.0, 0.25, 0.5, 0.75, 0.85)
 # ---------------------------------------------------------------------------
 
 
-def make_layer0(seed: int = 2605):
+def make_layer0(seed: int = 2605, shape=None, wdtype=None):
     """Layer weights from a seeded torch CPU generator: router [d,N] fp32 with
-    row 0 zeroed (constant channel carries no routing signal), experts bf16,
-    mask router rows 1.. ~ N(0, 1/d) (row 0 = theta, set per sparsity)."""
+    row 0 zeroed (constant channel carries no routing signal), experts bf16 (or
+    `wdtype`), mask router rows 1.. ~ N(0, 1/d) (row 0 = theta, set per sparsity)."""
     import torch
 
-    d, f, n = Q30["d"], Q30["f"], Q30["n"]
+    shape = shape or Q30
+    wdtype = wdtype or torch.bfloat16
+    d, f, n = shape["d"], shape["f"], shape["n"]
     g = torch.Generator().manual_seed(seed)
     router = torch.empty(d, n).normal_(0.0, 0.02, generator=g)
     router[0] = 0.0
-    wg = torch.empty(n, d, f).normal_(0.0, 0.02, generator=g).to(torch.bfloat16)
-    wu = torch.empty(n, d, f).normal_(0.0, 0.02, generator=g).to(torch.bfloat16)
-    wd = torch.empty(n, f, d).normal_(0.0, 0.02, generator=g).to(torch.bfloat16)
+    wg = torch.empty(n, d, f).normal_(0.0, 0.02, generator=g).to(wdtype)
+    wu = torch.empty(n, d, f).normal_(0.0, 0.02, generator=g).to(wdtype)
+    wd = torch.empty(n, f, d).normal_(0.0, 0.02, generator=g).to(wdtype)
     mask = torch.empty(d, n).normal_(0.0, 1.0 / math.sqrt(d), generator=g)
     mask[0] = 0.0
     return dict(router=router, wg=wg, wu=wu, wd=wd, mask=mask)
 
 
-def make_tokens(t: int, seed: int):
-    """h ~ N(0,1) with channel 0 held at 8, rounded to bf16."""
+def make_tokens(t: int, seed: int, d: int = Q30["d"], dtype=None):
+    """h ~ N(0,1) with channel 0 held at 8, rounded to bf16
+    (or kept in `dtype`, e.g. fp32 for the tiny config)."""
     import torch
 
     g = torch.Generator().manual_seed(seed)
-    h = torch.empty(t, Q30["d"]).normal_(0.0, 1.0, generator=g)
+    h = torch.empty(t, d).normal_(0.0, 1.0, generator=g)
     h[:, 0] = 8.0
-    return h.to(torch.bfloat16)
+    return h.to(dtype if dtype is not None else torch.bfloat16)
 
 
 def calibrate_theta(h_bf16, router, mask, k: int, s: float) -> float:
@@ -203,7 +206,7 @@ def cpu_cores_used():
 # ---------------------------------------------------------------------------
 
 
-def reference_block(w, theta: float):
+def reference_block(w, theta: float, shape=None):
     from oracle import ref
 
     beamoe = ref.import_beamoe()
@@ -211,7 +214,8 @@ def reference_block(w, theta: float):
     from beamoe.moe import Expert, MoEBlock, MoEBlockConfig
     from beamoe.tensor import Tensor
 
-    cfg = MoEBlockConfig(d_h=Q30["d"], d_ff=Q30["f"], num_experts=Q30["n"], top_k=Q30["k"])
+    shape = shape or Q30
+    cfg = MoEBlockConfig(d_h=shape["d"], d_ff=shape["f"], num_experts=shape["n"], top_k=shape["k"])
     rb = MoEBlock.__new__(MoEBlock)
     rb.cfg = cfg
     rb.router_w = Tensor._raw(w["router"].double().numpy())
@@ -225,8 +229,8 @@ def reference_block(w, theta: float):
     return beamoe, rb
 
 
-def time_reference(w, h_bf16, theta, budget_s: float, min_reps: int = 2, max_reps: int = 50):
-    beamoe, rb = reference_block(w, theta)
+def time_reference(w, h_bf16, theta, budget_s: float, min_reps: int = 2, max_reps: int = 50, shape=None):
+    beamoe, rb = reference_block(w, theta, shape)
     from beamoe.beam import beam_block_forward
     from beamoe.tensor import Tensor
 
@@ -330,13 +334,13 @@ class GpuLayer:
         self.graph.replay()
 
 
-def algorithmic_bytes(t, s_real, e_act, r, d, f, n):
+def algorithmic_bytes(t, s_real, e_act, r, d, f, n, k=Q30["k"], wbytes=2, xbytes=2):
     """Bytes the layer must move (bf16 experts, fp32 routers): activated experts'
     weights + router/mask weights + tokens in/out (+ small metadata)."""
-    w_exp = e_act * 3 * d * f * 2
+    w_exp = e_act * 3 * d * f * wbytes
     w_gate = 2 * n * d * 4
-    act = t * d * 2 * 2
-    meta = t * Q30["k"] * 8 * 2
+    act = t * d * xbytes * 2
+    meta = t * k * 8 * 2
     return w_exp + w_gate + act + meta
 
 
@@ -361,9 +365,10 @@ def timed_steps(layer, steps, flush, use_graph=True):
 def run_point(B, w, t, s, steps, warmup, flush, dev, seed=7, block_size=16):
     import torch
 
-    h = make_tokens(t, seed)
-    theta = calibrate_theta(h, w["router"], w["mask"], Q30["k"], s)
     blk = w["_block"]
+    k = blk.cfg.top_k
+    h = make_tokens(t, seed, blk.cfg.d_h, w.get("_xdtype"))
+    theta = calibrate_theta(h, w["router"], w["mask"], k, s)
     blk.mask_router.weight.copy_(mask_with_theta(w["mask"], theta).to(dev))
     x = h.to(dev)
     layer = GpuLayer(blk, x, block_size)
@@ -374,8 +379,83 @@ def run_point(B, w, t, s, steps, warmup, flush, dev, seed=7, block_size=16):
     mids = layer.outs["masked_ids"]
     r = int((mids >= 0).sum())
     e_act = int(torch.unique(mids[mids >= 0]).numel())
-    s_real = 1.0 - r / (t * Q30["k"])
+    s_real = 1.0 - r / (t * k)
     return dict(layer=layer, theta=theta, h=h, ms=float(np.mean(ms)), r=r, e_act=e_act, s_real=s_real)
+
+
+SHAPES = {  # BASELINE.json configs[0], [3], [4] (single-GPU layer; EP lines come from --gpus N)
+    "tiny": dict(d=256, f=512, n=8, k=2),
+    "olmoe": dict(d=2048, f=1024, n=64, k=8),
+    "q235": dict(d=4096, f=1536, n=128, k=8),
+}
+
+
+def shape_layer(B, name, dev):
+    """A block of one of the other BASELINE shapes.  tiny: fp32 experts and
+    tokens from the CPU generator (so the reference can run the same weights);
+    OLMoE / Q235: bf16 experts drawn on the device (MoEBlock.random, N(0, 0.02)),
+    router row 0 zeroed and the mask router drawn as for Q30."""
+    import torch
+
+    sh = SHAPES[name]
+    cfg = B.MoEBlockConfig(d_h=sh["d"], d_ff=sh["f"], num_experts=sh["n"], top_k=sh["k"])
+    if name == "tiny":
+        w = make_layer0(26050, sh, torch.float32)
+        w["_block"] = B.MoEBlock.from_weights(cfg, w["router"], (w["wg"], w["wu"], w["wd"]), mask_w=w["mask"],
+                                              dtype=torch.float32, device=dev)
+        w["_xdtype"] = torch.float32
+        return w
+    blk = B.MoEBlock.random(cfg, seed=2605, dtype=torch.bfloat16, device=dev)
+    with torch.no_grad():
+        blk.router_w[0].zero_()
+    g = torch.Generator().manual_seed(2606)
+    mask = torch.empty(sh["d"], sh["n"]).normal_(0.0, 1.0 / math.sqrt(sh["d"]), generator=g)
+    mask[0] = 0.0
+    blk.mask_router = B.MaskRouter(mask.to(dev))
+    return dict(router=blk.router_w.cpu(), mask=mask, _block=blk)
+
+
+def run_shapes(B, args, flush, dev, hbm_peak, tc_peak_sus):
+    """Decode T in {1, 64} and prefill T = 8192 across the sparsity range for the
+    OLMoE and Qwen3-235B layer shapes, and the tiny fp32 config (T = 1024) with
+    the reference's own CPU time and the parity of the same call beside it."""
+    import torch
+
+    rows = []
+    plan = {"tiny": [(1024, 0.0), (1024, 0.5)],
+            "olmoe": [(1, 0.0), (1, 0.5), (1, 0.85), (64, 0.0), (64, 0.5), (64, 0.85), (8192, 0.0), (8192, 0.85)],
+            "q235": [(1, 0.0), (1, 0.5), (1, 0.85), (64, 0.0), (64, 0.5), (64, 0.85), (8192, 0.0), (8192, 0.85)]}
+    for name, points in plan.items():
+        sh = SHAPES[name]
+        d, f, n, k = sh["d"], sh["f"], sh["n"], sh["k"]
+        w = shape_layer(B, name, dev)
+        wb = 4 if name == "tiny" else 2
+        for t, s in points:
+            steps = args.sweep_steps if t <= 1024 else 3
+            p = run_point(B, w, t, s, steps, 2, flush, dev, seed=7 if t <= 1024 else 11)
+            sec = p["ms"] * 1e-3
+            byt = algorithmic_bytes(t, p["s_real"], p["e_act"], p["r"], d, f, n, k, wbytes=wb, xbytes=wb)
+            flops = 6 * d * f * p["r"]
+            row = {"shape": name, **sh, "T": t, "s_target": s, "s_actual": round(p["s_real"], 4),
+                   "E_act": p["e_act"], "us_per_step": round(p["ms"] * 1e3, 2), "tokens_per_s": round(t / sec, 1),
+                   "layer_bytes": byt, "hbm_gbs": round(byt / sec / 1e9, 1),
+                   "hbm_frac_of_measured": round(byt / sec / 1e9 / hbm_peak, 4),
+                   "hbm_frac_of_8tbs": round(byt / sec / 1e9 / 8000.0, 4),
+                   "expert_tflops": round(flops / sec / 1e12, 2),
+                   "tensor_frac_of_sustained": round(flops / sec / 1e12 / tc_peak_sus, 4),
+                   "dtype": "f32" if name == "tiny" else "bf16"}
+            if name == "tiny" and not args.no_cpu:
+                ref_s, reps, ref_out = time_reference(w, p["h"], p["theta"], budget_s=min(args.cpu_budget, 5.0),
+                                                      shape=sh)
+                ours = p["layer"].outs["out"].float().cpu().double().numpy()
+                row["reference_cpu_us"] = round(ref_s * 1e6, 1)
+                row["reference_reps"] = reps
+                row["parity_vs_reference_max_rel_err"] = float(np.abs(ours - ref_out).max() / np.abs(ref_out).max())
+            rows.append(row)
+            del p
+        del w
+        torch.cuda.empty_cache()
+    return rows
 
 
 def run_lm_decode(args, new_tokens: int = 48):
@@ -519,7 +599,8 @@ def run_ours(args):
                 byt = algorithmic_bytes(tt, p["s_real"], p["e_act"], p["r"], d, f, n)
                 sweep.append({"T": tt, "s_target": ss, "s_actual": round(p["s_real"], 4), "E_act": p["e_act"],
                               "us_per_step": round(p["ms"] * 1e3, 2), "tokens_per_s": round(tt / (p["ms"] / 1e3), 1),
-                              "layer_bytes": byt, "hbm_frac_of_measured": round(byt / (p["ms"] * 1e-3) / 1e9 / hbm_peak, 4)})
+                              "layer_bytes": byt, "hbm_frac_of_measured": round(byt / (p["ms"] * 1e-3) / 1e9 / hbm_peak, 4),
+                              "hbm_frac_of_8tbs": round(byt / (p["ms"] * 1e-3) / 1e9 / 8000.0, 4)})
                 del p
         if not args.no_prefill:
             for ss in (0.0, 0.5, 0.85):
@@ -535,6 +616,9 @@ def run_ours(args):
                               "tensor_frac_of_sustained": round(flops / sec / 1e12 / tc_peak_sus, 4),
                               "hbm_frac_of_measured": round(byt / sec / 1e9 / hbm_peak, 4)})
                 del p
+
+    # ---- the other BASELINE shapes (tiny fp32, OLMoE, Qwen3-235B) ------------------
+    shapes = [] if args.no_shapes else run_shapes(B, args, flush, dev, hbm_peak, tc_peak_sus)
 
     # ---- mask-router training step: forward over all K candidates
     #      + fused slot-dot / closed-form STE backward + x_n^T dA (cuBLAS) ---------
@@ -584,6 +668,7 @@ def run_ours(args):
                 "path": "paper_2605_14438_b200.beam_block_forward(pinned host h) -> host outputs"},
         "roofline": {"bound": "hbm", "kernel": "gateup_kernel (experts gate/up, weight streaming)",
                      "achieved": gu_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gu_gbs / hbm_peak,
+                     "frac_of_8tbs": gu_gbs / 8000.0,
                      "peak_kind": peak_kind + " (copy bandwidth, MEASURED_PEAKS.json hbm_gbs)",
                      "traffic": ncu_traffic("gateup_warp_kernel" if t > 2 else "gateup_cta_kernel", f"T={t} s={s}"),
                      "algorithmic_bytes_per_launch": gu_bytes,
@@ -598,6 +683,7 @@ def run_ours(args):
         "gpu_launches_per_step": launches_per_step,
         "gpu_launches_counted_total": int(launches),
         "sweep": sweep,
+        "shapes": shapes,
         "train_mask_router": train,
         "lm_greedy_decode": lm_line,
     }
@@ -618,6 +704,7 @@ def main():
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--no-shapes", action="store_true", help="skip the tiny / OLMoE / Qwen3-235B shape lines")
     ap.add_argument("--expert-path", default="auto", choices=("auto", "simt", "tc", "tc1", "stream"),
                     help="expert-stage kernels (diagnostics; default auto)")
     args = ap.parse_args()

@@ -208,6 +208,89 @@ class EPBeamLayer:
 # ---------------------------------------------------------------------------
 
 
+def _capture_step(layer, x, dev):
+    """Decode-sized steps (fixed-capacity exchange: no host sync) replay as one
+    CUDA graph, NCCL collectives included — the eager step is host-launch bound.
+    Returns (graph, graph output) or (None, None) when the step is not captured."""
+    if x.shape[0] > FIXED_CAPACITY_MAX_T or os.environ.get("BEAM_EP_NO_GRAPH") == "1":
+        return None, None
+    try:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                layer.forward(x)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):  # the warmed-up stream: no workspace fill captured
+            y_graph = layer.forward(x)
+        torch.cuda.synchronize()
+        graph.replay()
+        torch.cuda.synchronize()
+        ref = layer.forward(x)
+        if not torch.equal(ref, y_graph):
+            return None, None  # not replay-safe here: time the eager step
+        return graph, y_graph
+    except Exception:  # capture unsupported by this NCCL / torch combination
+        torch.cuda.synchronize()
+        return None, None
+
+
+def _timed_total(step, steps, flush):
+    """Sum of per-step CUDA-event times (ms) on this rank, L2 flushed and ranks
+    barriered before every step."""
+    total = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        step()
+        e.record()
+        e.synchronize()
+        total += s.elapsed_time(e)
+    return total
+
+
+def _ep_shape_points(args, bench, dev, flush, world, rank):
+    """EP lines for the other BASELINE shapes (configs[3] OLMoE, configs[4]
+    Qwen3-235B): device ms per step, max over ranks, T tokens per rank."""
+    import paper_2605_14438_b200 as B
+
+    rows = []
+    for name, t, s in (("olmoe", 64, 0.5), ("olmoe", 8192, 0.5), ("q235", 1, 0.85), ("q235", 64, 0.85),
+                       ("q235", 8192, 0.85)):
+        sh = bench.SHAPES[name]
+        if sh["n"] % world:
+            continue
+        w = bench.shape_layer(B, name, dev)
+        blk = w["_block"]
+        theta = bench.calibrate_theta(bench.make_tokens(t, 7, sh["d"]), w["router"], w["mask"], sh["k"], s)
+        blk.mask_router.weight.copy_(bench.mask_with_theta(w["mask"], theta).to(dev))
+        layer = EPBeamLayer(blk)
+        blk.w_gu = torch.zeros(1, dtype=torch.bfloat16, device=dev)
+        blk.w_down = torch.zeros(1, dtype=torch.bfloat16, device=dev)
+        x = bench.make_tokens(t, 7 + rank, sh["d"]).to(dev)
+        for _ in range(2):
+            layer.forward(x)
+        torch.cuda.synchronize()
+        graph, _ = _capture_step(layer, x, dev)
+        step = graph.replay if graph is not None else (lambda: layer.forward(x))
+        steps = 10 if t <= 256 else 3
+        dist.barrier()
+        t_max = torch.tensor([_timed_total(step, steps, flush)], device=dev)
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        ms = float(t_max.item()) / steps
+        rows.append({"shape": name, **sh, "T_per_rank": t, "s_target": s, "ep": world,
+                     "experts_per_rank": sh["n"] // world, "ms_per_step": round(ms, 4),
+                     "tokens_per_s": round(world * t / (ms / 1e3), 1), "graph": graph is not None})
+        del layer, blk, w, graph, step
+        torch.cuda.empty_cache()
+    return rows
+
+
 def bench_main(args, bench):
     import json
 
@@ -243,44 +326,11 @@ def bench_main(args, bench):
     layer.forward(x)  # launches of one step through the C ABI (gate + local experts)
     torch.cuda.synchronize()
     launches_per_step = int(lib.beam_kernel_launches() - c0)
-    # decode-sized steps (fixed-capacity exchange: no host sync) replay as one CUDA
-    # graph, NCCL collectives included — the eager step is host-launch bound
-    graph, y_graph = None, None
-    if x.shape[0] <= FIXED_CAPACITY_MAX_T and os.environ.get("BEAM_EP_NO_GRAPH") != "1":
-        try:
-            side = torch.cuda.Stream(dev)
-            side.wait_stream(torch.cuda.current_stream(dev))
-            with torch.cuda.stream(side):
-                for _ in range(2):
-                    layer.forward(x)
-            torch.cuda.current_stream(dev).wait_stream(side)
-            torch.cuda.synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=side):  # the warmed-up stream: no workspace fill captured
-                y_graph = layer.forward(x)
-            torch.cuda.synchronize()
-            graph.replay()
-            torch.cuda.synchronize()
-            ref = layer.forward(x)
-            if not torch.equal(ref, y_graph):
-                graph = None  # not replay-safe here: time the eager step
-        except Exception:  # capture unsupported by this NCCL / torch combination
-            graph = None
-            torch.cuda.synchronize()
+    graph, y_graph = _capture_step(layer, x, dev)
     step = graph.replay if graph is not None else (lambda: layer.forward(x))
     dist.barrier()
-    total = 0.0
     with bench.ClockSampler(dev.index) as clocks:
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            dist.barrier()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            step()
-            e.record()
-            e.synchronize()
-            total += s.elapsed_time(e)
+        total = _timed_total(step, args.steps, flush)
     t_max = torch.tensor([total], device=dev)
     dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item()) / args.steps
@@ -305,6 +355,7 @@ def bench_main(args, bench):
     e2e_max = torch.tensor([e2e_total], device=dev)
     dist.all_reduce(e2e_max, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e_max.item()) / args.steps
+    shape_rows = [] if getattr(args, "no_shapes", False) else _ep_shape_points(args, bench, dev, flush, world, rank)
     if rank == 0:
         line = {
             "metric": bench.METRIC, "value": world * args.tokens / (ms / 1e3), "unit": "tokens/s",
@@ -327,6 +378,7 @@ def bench_main(args, bench):
             "clocks": clocks.summary(),
             "gpu_launches": launches_per_step * args.steps,
             "gpu_launches_per_step": launches_per_step,
+            "shapes": shape_rows,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
