@@ -90,6 +90,7 @@ struct LayerWs {
   PlanDev plan;
   float* act;
   float* opair;
+  float* xw;       // [T, d_pad] x * norm_w, fp32 (decode: written by the fused gate)
 };
 
 // One layout serves every entry (sized for the largest user, beam_layer_forward).
@@ -125,6 +126,7 @@ static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, La
   w.plan.slot_expert = c.take<int32_t>(M);
   w.act = w.tc ? nullptr : c.take<float>(cap * g.f_pad);
   w.opair = c.take<float>(cap * g.d_pad);
+  w.xw = (T <= 64 && L.has_norm) ? c.take<float>((size_t)T * g.d_pad) : nullptr;
   if (o) *o = w;
   return c.off + 256;
 }
@@ -331,10 +333,15 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
     for (int m = 1; m < kStageMarks; ++m) prof_mark(m, s);
     return BEAM_OK;
   }
+  // decode with an RMS norm: the fused gate also writes x * norm_w (fp32) for the
+  // weight-streaming expert kernels
+  const bool prescaled = L.has_norm && w.xw != nullptr && !w.tc && g_expert_path.load() != 4 &&
+                         gate_fused_supported(T, g.N, g.E, g.d_pad);
   if (gate_fused_supported(T, g.N, g.E, g.d_pad)) {
     // decode: projection + top-K + permute in one launch
     BEAM_TRY(launch_gate_fused(X, h_dtype, L.has_norm ? L.norm_w : nullptr, L.gate_wT, T, g.d, g.d_pad,
-                               w.logits2, topk_args(L, g, o, w, sp), g.E, block_size, w.tc, w.plan, w.counters, s));
+                               w.logits2, topk_args(L, g, o, w, sp), g.E, block_size, w.tc, w.plan, w.counters, s,
+                               prescaled ? w.xw : nullptr));
     prof_mark(1, s);
   } else {
     BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s, sp));
@@ -356,8 +363,11 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
     BEAM_TRY(launch_down_stream(L, g, w.plan, w.act, w.opair, s));
     prof_mark(4, s);
   } else {
-    BEAM_TRY(launch_gateup_simt(L, g, X, h_dtype, T, L.has_norm ? w.inv : nullptr,
-                                L.has_norm ? L.norm_w : nullptr, w.plan, w.act, s));
+    if (prescaled)
+      BEAM_TRY(launch_gateup_simt(L, g, w.xw, BEAM_F32, T, w.inv, nullptr, w.plan, w.act, s));
+    else
+      BEAM_TRY(launch_gateup_simt(L, g, X, h_dtype, T, L.has_norm ? w.inv : nullptr,
+                                  L.has_norm ? L.norm_w : nullptr, w.plan, w.act, s));
     prof_mark(3, s);
     BEAM_TRY(launch_down_simt(L, g, T, w.plan, w.act, w.opair, s));
     prof_mark(4, s);

@@ -109,7 +109,8 @@ cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dt
 bool gate_fused_supported(int T, int N, int E, int d_pad);
 cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, const float* gate_wT, int T,
                               int d, int d_pad, float* P, const TopkArgs& a, int E, int bs,
-                              bool pad, const PlanDev& p, int* counters, cudaStream_t s);
+                              bool pad, const PlanDev& p, int* counters, cudaStream_t s,
+                              float* xw = nullptr);  // xw: [T, d_pad] x * norm_w (fp32) when norm_w is set
 cudaError_t launch_mask_route(const int64_t* ids, const void* a, int a_dtype, int T, int K,
                               int N, int64_t* out, cudaStream_t s);
 

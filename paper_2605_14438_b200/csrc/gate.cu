@@ -174,7 +174,8 @@ template <typename TX, int TT>
 __device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const float* __restrict__ nw,
                                                  const float* __restrict__ W, int T, int cols, int d,
                                                  int d_pad, int kr, float* __restrict__ P, float* xs,
-                                                 float* red_s, float* __restrict__ ssp = nullptr) {
+                                                 float* red_s, float* __restrict__ ssp = nullptr,
+                                                 float* __restrict__ xw = nullptr) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int c0 = (blockIdx.x * 8 + wib) * kGemvCols;
   const int split = blockIdx.y;
@@ -215,6 +216,18 @@ __device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const
       }
       q = warp_sum(q);
       if (lane == 0) ssp[(size_t)split * T + t0 + t] = q;
+    }
+    if (xw != nullptr) {
+      // the norm-weighted token rows x * w (fp32, exactly the product the decode
+      // gate/up kernels formed per chunk) for the expert stage: its inner loop
+      // then loads one row per token and does no per-chunk norm multiply
+      for (int v = threadIdx.x; v < nt * (kn >> 2); v += 256) {
+        const int t = v / (kn >> 2), k4 = v % (kn >> 2);
+        const float4 x = *reinterpret_cast<const float4*>(xs + t * kr + 4 * k4);
+        const float4 g = ld_norm4(nw, ks + 4 * k4, d);
+        *reinterpret_cast<float4*>(xw + (size_t)(t0 + t) * d_pad + ks + 4 * k4) =
+            make_float4(x.x * g.x, x.y * g.y, x.z * g.z, x.w * g.w);
+      }
     }
   }
   float acc[kGemvCols * TT];
@@ -379,14 +392,15 @@ template <typename TX, int NPL, int KIND>
 __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ X, const float* __restrict__ nw,
                                                          const float* __restrict__ W, int T, int d, int d_pad,
                                                          int kr, float* __restrict__ P, TopkArgs a, int E,
-                                                         int bs, bool pad, PlanDev p, int* __restrict__ counters) {
+                                                         int bs, bool pad, PlanDev p, int* __restrict__ counters,
+                                                         float* __restrict__ xw) {
   extern __shared__ float xs[];  // phase 1: token tile; phase 3: permute scratch
   __shared__ float red_s[8 * kGemvCols * kFusedTT];
   __shared__ int s_last;
   const int cols = a.cols;
   float* ssp = nw != nullptr ? P + (size_t)kFusedMaxSplit * T * cols : nullptr;
   trace_minmax(0, 1);
-  router_gemv_body<TX, kFusedTT>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s, ssp);
+  router_gemv_body<TX, kFusedTT>(X, nw, W, T, cols, d, d_pad, kr, P, xs, red_s, ssp, xw);
   trace_minmax(2, 3);
 
   // ---- last CTA of this token tile: top-K + mask ----
@@ -451,19 +465,20 @@ bool gate_fused_supported(int T, int N, int E, int d_pad) {
 template <typename TX, int NPL, int KIND>
 static cudaError_t fused_launch(dim3 grid, size_t smem, const void* X, const float* nw, const float* W, int T,
                                 int d, int d_pad, int kr, float* P, const TopkArgs& a, int E, int bs,
-                                bool pad, const PlanDev& p, int* counters, cudaStream_t s) {
+                                bool pad, const PlanDev& p, int* counters, float* xw, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     set_smem(gate_fused_kernel<TX, NPL, KIND>, 160 * 1024);
     attr = true;
   }
-  gate_fused_kernel<TX, NPL, KIND><<<grid, 256, smem, s>>>((const TX*)X, nw, W, T, d, d_pad, kr, P, a, E, bs, pad, p, counters);
+  gate_fused_kernel<TX, NPL, KIND><<<grid, 256, smem, s>>>((const TX*)X, nw, W, T, d, d_pad, kr, P, a, E, bs, pad, p, counters,
+                                                            nw != nullptr ? xw : nullptr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, const float* gate_wT, int T,
                               int d, int d_pad, float* P, const TopkArgs& a, int E, int bs,
-                              bool pad, const PlanDev& p, int* counters, cudaStream_t s) {
+                              bool pad, const PlanDev& p, int* counters, cudaStream_t s, float* xw) {
   const int cols = a.cols;
   const int kr = gemv_kr(T, cols, d_pad, kFusedMaxSplit, kFusedTT);
   dim3 grid(ceil_div(cols, 8 * kGemvCols), ceil_div(d_pad, kr), ceil_div(T, kFusedTT));
@@ -472,11 +487,11 @@ cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, c
   const int npl = ceil_div(a.Nr, 32);
   cudaError_t e;
 #define BEAM_FUSED(TX_, K_)                                                                                    \
-  if (npl <= 1) e = fused_launch<TX_, 1, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
-  else if (npl <= 2) e = fused_launch<TX_, 2, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
-  else if (npl <= 4) e = fused_launch<TX_, 4, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
-  else if (npl <= 8) e = fused_launch<TX_, 8, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s); \
-  else e = fused_launch<TX_, 16, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, s);
+  if (npl <= 1) e = fused_launch<TX_, 1, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, xw, s); \
+  else if (npl <= 2) e = fused_launch<TX_, 2, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, xw, s); \
+  else if (npl <= 4) e = fused_launch<TX_, 4, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, xw, s); \
+  else if (npl <= 8) e = fused_launch<TX_, 8, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, xw, s); \
+  else e = fused_launch<TX_, 16, K_>(grid, smem, X, norm_w, gate_wT, T, d, d_pad, kr, P, a, E, bs, pad, p, counters, xw, s);
   const bool beam = a.kind == BEAM_ROUTE_BEAM && a.Nr == a.N && a.cols == 2 * a.N && a.mask_off == a.N;
   if (x_dtype == BEAM_BF16) {
     if (beam) { BEAM_FUSED(__nv_bfloat16, BEAM_ROUTE_BEAM) } else { BEAM_FUSED(__nv_bfloat16, -1) }
