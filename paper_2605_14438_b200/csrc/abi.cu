@@ -364,7 +364,7 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
     prof_mark(4, s);
   } else {
     if (prescaled)
-      BEAM_TRY(launch_gateup_simt(L, g, w.xw, BEAM_F32, T, w.inv, nullptr, w.plan, w.act, s));
+      BEAM_TRY(launch_gateup_simt(L, g, w.xw, BEAM_F32, T, w.inv, nullptr, w.plan, w.act, s, (long long)T * sp.Keff));
     else
       BEAM_TRY(launch_gateup_simt(L, g, X, h_dtype, T, L.has_norm ? w.inv : nullptr,
                                   L.has_norm ? L.norm_w : nullptr, w.plan, w.act, s));

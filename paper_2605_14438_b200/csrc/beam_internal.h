@@ -127,11 +127,13 @@ cudaError_t launch_plan_prepare(const int32_t* counts, const int32_t* offsets,
                                 const PlanDev& p, int32_t* flags, cudaStream_t s);
 
 // experts_simt.cu
+// slots: planned (token, slot) entries when the caller knows them (T * Keff),
+// -1 = unknown; only prunes the MMA launch, never changes results
 cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
                                const float* inv, const float* nw, const PlanDev& p, float* act,
-                               cudaStream_t s);
+                               cudaStream_t s, long long slots = -1);
 cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const PlanDev& p,
-                             const float* act, float* opair, cudaStream_t s);
+                             const float* act, float* opair, cudaStream_t s, long long slots = -1);
 // experts_stream.cu (bulk-copy weight streaming, bf16 weights)
 bool stream_supported(const beam_layer_t& L, const Dims& g);
 cudaError_t launch_gateup_stream(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype,

@@ -16,6 +16,9 @@
 // (deterministic, independent of the grid).  Two launches:
 //   gateup: 4 gate + 4 up rows per item -> act[pos, f] = act(g) * u   (fp32)
 //   down:   2 x 8 output rows per item  -> opair[pos, d] = ghat * (act . W_down)
+#include <cstdlib>
+#include <type_traits>
+
 #include "beam_common.cuh"
 #include "beam_internal.h"
 
@@ -306,16 +309,12 @@ __device__ __forceinline__ void gateup_warp_tile(const TW* __restrict__ W, int r
 }
 
 template <typename TW, typename TX, int ACT>
-__global__ void __launch_bounds__(kThreads, 2) gateup_warp_kernel(const TW* __restrict__ Wgu,
-                                                                  const TX* __restrict__ X,
-                                                                  const float* __restrict__ inv,
-                                                                  const float* __restrict__ nw, int d,
-                                                                  int d_pad, int f_pad, PlanDev p,
-                                                                  float* __restrict__ act) {
-  __shared__ float red_s[kWarps][32];
+__device__ __forceinline__ void gateup_warp_items(const TW* __restrict__ Wgu, const TX* __restrict__ X,
+                                                  const float* __restrict__ inv, const float* __restrict__ nw,
+                                                  int d, int d_pad, int f_pad, PlanDev p,
+                                                  float* __restrict__ act, float (*red_s)[32]) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * kWarps + wib, nwarps = gridDim.x * kWarps;
-  griddep_wait();
   const int groups = f_pad / 4;
   const long long total = (long long)p.meta[0] * groups;
   for (long long item = gwarp; item < total; item += nwarps) {
@@ -342,6 +341,18 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_warp_kernel(const TW* __re
       }
     }
   }
+}
+
+template <typename TW, typename TX, int ACT>
+__global__ void __launch_bounds__(kThreads, 2) gateup_warp_kernel(const TW* __restrict__ Wgu,
+                                                                  const TX* __restrict__ X,
+                                                                  const float* __restrict__ inv,
+                                                                  const float* __restrict__ nw, int d,
+                                                                  int d_pad, int f_pad, PlanDev p,
+                                                                  float* __restrict__ act) {
+  __shared__ float red_s[kWarps][32];
+  griddep_wait();
+  gateup_warp_items<TW, TX, ACT>(Wgu, X, inv, nw, d, d_pad, f_pad, p, act, red_s);
 }
 
 template <typename TW, int TB>
@@ -392,14 +403,11 @@ __device__ __forceinline__ void down_warp_tile(const TW* __restrict__ W, int row
 }
 
 template <typename TW>
-__global__ void __launch_bounds__(kThreads, 2) down_warp_kernel(const TW* __restrict__ Wd,
-                                                                const float* __restrict__ act, int d_pad,
-                                                                int f_pad, PlanDev p,
-                                                                float* __restrict__ opair) {
-  __shared__ float red_s[kWarps][32];
+__device__ __forceinline__ void down_warp_items(const TW* __restrict__ Wd, const float* __restrict__ act, int d_pad,
+                                                int f_pad, PlanDev p, float* __restrict__ opair,
+                                                float (*red_s)[32]) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * kWarps + wib, nwarps = gridDim.x * kWarps;
-  griddep_wait();
   const int groups = d_pad / 8;
   const long long total = (long long)p.meta[0] * groups;
   for (long long item = gwarp; item < total; item += nwarps) {
@@ -426,18 +434,280 @@ __global__ void __launch_bounds__(kThreads, 2) down_warp_kernel(const TW* __rest
   }
 }
 
+template <typename TW>
+__global__ void __launch_bounds__(kThreads, 2) down_warp_kernel(const TW* __restrict__ Wd,
+                                                                const float* __restrict__ act, int d_pad,
+                                                                int f_pad, PlanDev p,
+                                                                float* __restrict__ opair) {
+  __shared__ float red_s[kWarps][32];
+  griddep_wait();
+  down_warp_items<TW>(Wd, act, d_pad, f_pad, p, opair, red_s);
+}
+
+// ---------------------------------------------------------------------------
+// tensor-core warp-item kernels (bf16 weights, no in-kernel norm multiply; T > 2):
+// the same weight stream, but the multiply-adds run on mma.sync m16n8k16 (one
+// instruction per 16 x 8 x 16 MACs instead of FFMA2s + bf16 unpacking), so a
+// warp spends its issue slots on loads.  A warp item is 16 weight rows (8 gate +
+// 8 up rows of 8 features, or 16 down rows) x up to 8 tokens per pass.  Each
+// lane streams 16 contiguous bytes of two rows per 32-k step straight into its
+// A fragment: the k order inside a step is permuted identically for A and B,
+// which a dot product does not see.  fp32 token operands are split x = hi + lo
+// into two bf16 terms (two MMAs, ~16 significant bits), so the result keeps the
+// FFMA kernels' accuracy; bf16 tokens are exact in one term.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// (x0, x1) -> bf16 pairs hi and lo with x ~= hi + lo
+__device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  hi = bf16x2(x0, x1);
+  lo = bf16x2(x0 - __uint_as_float(hi << 16), x1 - __uint_as_float(hi & 0xffff0000u));
+}
+
+// B operand of one 32-k step: this lane's 8 k values of its token row, as 4
+// bf16 pairs (hi) and, for fp32 rows, 4 residual pairs (lo)
+template <typename TX>
+struct BStep {
+  uint32_t hi[4], lo[4];
+};
+template <typename TX>
+__device__ __forceinline__ void load_bstep(const TX* p, bool ok, BStep<TX>& b) {
+  if constexpr (sizeof(TX) == 2) {
+    const uint4 v = ok ? ld_cached(p) : make_uint4(0u, 0u, 0u, 0u);
+    b.hi[0] = v.x; b.hi[1] = v.y; b.hi[2] = v.z; b.hi[3] = v.w;
+  } else {
+    float4 u = make_float4(0.f, 0.f, 0.f, 0.f), v = u;
+    if (ok) {
+      u = __ldg(reinterpret_cast<const float4*>(p));
+      v = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    }
+    split_pair(u.x, u.y, b.hi[0], b.lo[0]);
+    split_pair(u.z, u.w, b.hi[1], b.lo[1]);
+    split_pair(v.x, v.y, b.hi[2], b.lo[2]);
+    split_pair(v.z, v.w, b.hi[3], b.lo[3]);
+  }
+}
+// c += A(rows r0 | r1, this step) * B: two k16 MMAs per step (x2 for hi + lo)
+template <typename TX>
+__device__ __forceinline__ void mma_step(float (&c)[4], const uint4& w0, const uint4& w1, const BStep<TX>& b) {
+  mma_bf16_16816(c, w0.x, w1.x, w0.y, w1.y, b.hi[0], b.hi[1]);
+  mma_bf16_16816(c, w0.z, w1.z, w0.w, w1.w, b.hi[2], b.hi[3]);
+  if constexpr (sizeof(TX) == 4) {
+    mma_bf16_16816(c, w0.x, w1.x, w0.y, w1.y, b.lo[0], b.lo[1]);
+    mma_bf16_16816(c, w0.z, w1.z, w0.w, w1.w, b.lo[2], b.lo[3]);
+  }
+}
+
+constexpr int kMmaUnroll = 4;  // 32-k steps in flight per lane (4 x 32 B of weights); mma_rows sums 4 accumulators
+
+// rows r0 (lanes' group g) and r1 = r0 + gap of W [*, K] against the token rows
+// xrow (this lane's B token), over K in 32-element steps
+template <typename TX>
+__device__ __forceinline__ void mma_rows(const __nv_bfloat16* __restrict__ w0p, const __nv_bfloat16* __restrict__ w1p,
+                                         const TX* __restrict__ xrow, int K, int q, float (&c)[4]) {
+  const int steps = (K + 31) / 32;
+  // one accumulator per unrolled step: the MMAs of a step do not wait on the
+  // previous step's (fixed final summation order: deterministic)
+  float cu[kMmaUnroll][4];
+#pragma unroll
+  for (int u = 0; u < kMmaUnroll; ++u) cu[u][0] = cu[u][1] = cu[u][2] = cu[u][3] = 0.0f;
+  for (int s0 = 0; s0 < steps; s0 += kMmaUnroll) {
+    uint4 a0[kMmaUnroll], a1[kMmaUnroll];
+    BStep<TX> b[kMmaUnroll];
+#pragma unroll
+    for (int u = 0; u < kMmaUnroll; ++u) {
+      const int k = (s0 + u) * 32 + q * 8;
+      const bool ok = s0 + u < steps && k < K;
+      a0[u] = ok ? ld_stream(w0p + k) : make_uint4(0u, 0u, 0u, 0u);
+      a1[u] = ok ? ld_stream(w1p + k) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kMmaUnroll; ++u) {
+      const int k = (s0 + u) * 32 + q * 8;
+      load_bstep<TX>(xrow + k, s0 + u < steps && k < K, b[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kMmaUnroll; ++u) mma_step<TX>(cu[u], a0[u], a1[u], b[u]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = (cu[0][i] + cu[1][i]) + (cu[2][i] + cu[3][i]);
+}
+
+template <typename TX, int ACT>
+__device__ __forceinline__ void gateup_mma_items(const __nv_bfloat16* __restrict__ Wgu, const TX* __restrict__ X,
+                                                 const float* __restrict__ inv, int d_pad, int f_pad,
+                                                 PlanDev p, float* __restrict__ act) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5), nwarps = gridDim.x * kWarps;
+  const int groups = f_pad / 8;
+  const long long total = (long long)p.meta[0] * groups;
+  for (long long item = gwarp; item < total; item += nwarps) {
+    const int a = (int)(item / groups), gi = (int)(item % groups);
+    const int e = p.active[a];
+    const int cnt = p.counts[e], off = p.offsets[e];
+    const int feat0 = gi * 8;
+    // packed W_gu: per 16 features, 16 gate rows then 16 up rows
+    const int rg = (feat0 >> 4) * 32 + (feat0 & 15) + g;
+    const __nv_bfloat16* W = Wgu + (size_t)e * 2 * f_pad * d_pad;
+    for (int t0 = 0; t0 < cnt; t0 += 8) {
+      const int nt = min(8, cnt - t0);
+      const int* tokp = p.tok + off + t0;
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      mma_rows<TX>(W + (size_t)rg * d_pad, W + (size_t)(rg + 16) * d_pad, X + (size_t)tokp[g < nt ? g : 0] * d_pad,
+                   d_pad, q, c);
+      // c[0], c[1]: gate of feature feat0 + g for tokens 2q, 2q + 1; c[2], c[3]: up
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int n = 2 * q + j;
+        if (n < nt) {
+          const float s = inv ? inv[tokp[n]] : 1.0f;
+          act[(size_t)(off + t0 + n) * f_pad + feat0 + g] = activation<ACT>(c[j] * s) * (c[2 + j] * s);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void down_mma_items(const __nv_bfloat16* __restrict__ Wd, const float* __restrict__ act,
+                                               int d_pad, int f_pad, PlanDev p, float* __restrict__ opair) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5), nwarps = gridDim.x * kWarps;
+  const int groups = (d_pad + 15) / 16;
+  const long long total = (long long)p.meta[0] * groups;
+  for (long long item = gwarp; item < total; item += nwarps) {
+    const int a = (int)(item / groups), gi = (int)(item % groups);
+    const int e = p.active[a];
+    const int cnt = p.counts[e], off = p.offsets[e];
+    const int r0 = gi * 16 + g, r1 = r0 + 8;
+    const __nv_bfloat16* W = Wd + (size_t)e * d_pad * f_pad;
+    // rows past d_pad (d_pad % 16 == 8) read row d_pad - 1 and are not stored
+    const __nv_bfloat16* w0p = W + (size_t)min(r0, d_pad - 1) * f_pad;
+    const __nv_bfloat16* w1p = W + (size_t)min(r1, d_pad - 1) * f_pad;
+    for (int t0 = 0; t0 < cnt; t0 += 8) {
+      const int nt = min(8, cnt - t0);
+      const int pos0 = off + t0;
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      mma_rows<float>(w0p, w1p, act + (size_t)(pos0 + (g < nt ? g : 0)) * f_pad, f_pad, q, c);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int n = 2 * q + j;
+        if (n < nt) {
+          const float wn = p.w[pos0 + n];
+          if (r0 < d_pad) opair[(size_t)(pos0 + n) * d_pad + r0] = c[j] * wn;
+          if (r1 < d_pad) opair[(size_t)(pos0 + n) * d_pad + r1] = c[2 + j] * wn;
+        }
+      }
+    }
+  }
+}
+
+// Which item kernel runs is decided on the device from the plan: the MMA items
+// (16 rows x 8 tokens) pay off once experts carry enough surviving tokens on
+// average (R >= tok * E_act) and there are enough of them to give every warp >= 3
+// (they are 2x larger than the FFMA items, which otherwise keep more warps and
+// weight bytes in flight).  Q30 sweep on B200: T=64 s=0 347 -> 275 us, T=64
+// s=0.25 281 -> 251 us; T=16 s=0.25 (58 experts) 132 us FFMA vs 137 us MMA.
+__device__ __forceinline__ bool use_mma_items(const PlanDev& p, int items_per_expert, int tok_per_expert) {
+  const int e_act = p.meta[0];
+  return p.meta[2] >= tok_per_expert * e_act && (long long)e_act * items_per_expert >= 3LL * gridDim.x * kWarps;
+}
+// tokens per active expert from which the MMA items win: gate/up 3 (at 2.4 they
+// lose 4 %: T=64 s=0.5 gate/up 134 vs 129 us), down 2 (72 -> 68 us there)
+constexpr int kMmaTokGateUp = 3, kMmaTokDown = 2;
+
+// Two launches per stage, each leaving at once when the plan picks the other
+// (one kernel holding both bodies spills, or with 2-token FFMA passes runs the
+// FFMA items up to 15 % slower): MMA items first, then the FFMA items.  The host
+// skips the MMA launch when T * Keff rules it out (mma_possible).
+template <typename TX, int ACT>
+__global__ void __launch_bounds__(kThreads, 2) gateup_mma_kernel(const __nv_bfloat16* __restrict__ Wgu,
+                                                                 const TX* __restrict__ X,
+                                                                 const float* __restrict__ inv, int d_pad,
+                                                                 int f_pad, PlanDev p, float* __restrict__ act) {
+  griddep_wait();
+  if (use_mma_items(p, f_pad / 8, kMmaTokGateUp)) gateup_mma_items<TX, ACT>(Wgu, X, inv, d_pad, f_pad, p, act);
+}
+template <typename TX, int ACT>
+__global__ void __launch_bounds__(kThreads, 2) gateup_ffma_kernel(const __nv_bfloat16* __restrict__ Wgu,
+                                                                  const TX* __restrict__ X,
+                                                                  const float* __restrict__ inv,
+                                                                  const float* __restrict__ nw, int d,
+                                                                  int d_pad, int f_pad, PlanDev p,
+                                                                  float* __restrict__ act) {
+  // nw is always null here; a runtime argument keeps the register allocation of
+  // gateup_warp_kernel (a literal null makes ptxas spill)
+  __shared__ float red_s[kWarps][32];
+  griddep_wait();
+  if (!use_mma_items(p, f_pad / 8, kMmaTokGateUp))
+    gateup_warp_items<__nv_bfloat16, TX, ACT>(Wgu, X, inv, nw, d, d_pad, f_pad, p, act, red_s);
+}
+
+__global__ void __launch_bounds__(kThreads, 2) down_mma_kernel(const __nv_bfloat16* __restrict__ Wd,
+                                                               const float* __restrict__ act, int d_pad,
+                                                               int f_pad, PlanDev p, float* __restrict__ opair) {
+  griddep_wait();
+  if (use_mma_items(p, (d_pad + 15) / 16, kMmaTokDown)) down_mma_items(Wd, act, d_pad, f_pad, p, opair);
+}
+__global__ void __launch_bounds__(kThreads, 2) down_ffma_kernel(const __nv_bfloat16* __restrict__ Wd,
+                                                                const float* __restrict__ act, int d_pad,
+                                                                int f_pad, PlanDev p, float* __restrict__ opair) {
+  __shared__ float red_s[kWarps][32];
+  griddep_wait();
+  if (!use_mma_items(p, (d_pad + 15) / 16, kMmaTokDown)) down_warp_items<__nv_bfloat16>(Wd, act, d_pad, f_pad, p, opair, red_s);
+}
+
+// Host side of use_mma_items: E_act * items >= 3 * warps needs E_act >= e_min,
+// and R >= tok * E_act needs T * Keff >= R >= tok * e_min.
+static bool mma_possible(long long slots, int items_per_expert, int tok_per_expert, int grid) {
+  if (slots < 0) return true;  // unknown slot count: let the device decide
+  const long long e_min = (3LL * grid * kWarps + items_per_expert - 1) / items_per_expert;
+  return slots >= tok_per_expert * e_min;
+}
+
+// mma kernels: bf16 weights, token rows without a pending norm multiply
+// (BEAM_DECODE_MMA=0 keeps the FFMA kernels)
+static bool mma_enabled() {
+  static const int v = [] {
+    const char* e = getenv("BEAM_DECODE_MMA");
+    return e == nullptr ? 1 : atoi(e);
+  }();
+  return v != 0;
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 template <typename TW, typename TX>
 static void gateup_dispatch(const beam_layer_t& L, const Dims& g, const void* X, const float* inv,
                             const float* nw, const PlanDev& p, float* act, int grid, bool cta,
-                            cudaStream_t s) {
+                            long long slots, cudaStream_t s) {
   if (cta) {
     if (L.activation == BEAM_ACT_SILU)
       launch_pdl(gateup_cta_kernel<TW, TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, (const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
     else
       launch_pdl(gateup_cta_kernel<TW, TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, (const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+  } else if (std::is_same<TW, __nv_bfloat16>::value && nw == nullptr && mma_enabled()) {
+    const __nv_bfloat16* W = (const __nv_bfloat16*)L.w_gu;
+    const bool mma = mma_possible(slots, g.f_pad / 8, kMmaTokGateUp, grid);
+    if (L.activation == BEAM_ACT_SILU) {
+      if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act);
+      launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+    } else {
+      if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act);
+      launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+    }
+    if (mma) count_launches(1);
   } else {
     if (L.activation == BEAM_ACT_SILU)
       launch_pdl(gateup_warp_kernel<TW, TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, (const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
@@ -453,27 +723,33 @@ static bool small_batch(int T) { return T <= 2; }
 
 cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
                                const float* inv, const float* nw, const PlanDev& p, float* act,
-                               cudaStream_t s) {
+                               cudaStream_t s, long long slots) {
   const bool xb = x_dtype == BEAM_BF16;
   const bool cta = small_batch(T);
   const int grid = num_sms() * (cta ? kCtaPerSm : 2);
   if (L.wdtype == BEAM_BF16) {
-    if (xb) gateup_dispatch<__nv_bfloat16, __nv_bfloat16>(L, g, X, inv, nw, p, act, grid, cta, s);
-    else gateup_dispatch<__nv_bfloat16, float>(L, g, X, inv, nw, p, act, grid, cta, s);
+    if (xb) gateup_dispatch<__nv_bfloat16, __nv_bfloat16>(L, g, X, inv, nw, p, act, grid, cta, slots, s);
+    else gateup_dispatch<__nv_bfloat16, float>(L, g, X, inv, nw, p, act, grid, cta, slots, s);
   } else {
-    if (xb) gateup_dispatch<float, __nv_bfloat16>(L, g, X, inv, nw, p, act, grid, cta, s);
-    else gateup_dispatch<float, float>(L, g, X, inv, nw, p, act, grid, cta, s);
+    if (xb) gateup_dispatch<float, __nv_bfloat16>(L, g, X, inv, nw, p, act, grid, cta, slots, s);
+    else gateup_dispatch<float, float>(L, g, X, inv, nw, p, act, grid, cta, slots, s);
   }
   count_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const PlanDev& p,
-                             const float* act, float* opair, cudaStream_t s) {
+                             const float* act, float* opair, cudaStream_t s, long long slots) {
   const bool cta = small_batch(T);
   const int grid = num_sms() * (cta ? kCtaPerSm : 2);
   if (L.wdtype == BEAM_BF16) {
     if (cta) launch_pdl(down_cta_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+    else if (mma_enabled()) {
+      const bool mma = mma_possible(slots, (g.d_pad + 15) / 16, kMmaTokDown, grid);
+      if (mma) launch_pdl(down_mma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+      launch_pdl(down_ffma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+      if (mma) count_launches(1);
+    }
     else launch_pdl(down_warp_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
   } else {
     if (cta) launch_pdl(down_cta_kernel<float>, grid, kThreads, 0, s, (const float*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
