@@ -670,7 +670,7 @@ def run_ours(args):
                      "achieved": gu_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gu_gbs / hbm_peak,
                      "frac_of_8tbs": gu_gbs / 8000.0,
                      "peak_kind": peak_kind + " (copy bandwidth, MEASURED_PEAKS.json hbm_gbs)",
-                     "traffic": ncu_traffic("gateup_warp_kernel" if t > 2 else "gateup_cta_kernel", f"T={t} s={s}"),
+                     "traffic": ncu_traffic("gateup_ffma_kernel" if t > 2 else "gateup_cta_kernel", f"T={t} s={s}"),
                      "algorithmic_bytes_per_launch": gu_bytes,
                      "layer": {"bytes": layer_bytes, "achieved_gbs": layer_bytes / (ms * 1e-3) / 1e9,
                                "frac": layer_bytes / (ms * 1e-3) / 1e9 / hbm_peak},
