@@ -9,7 +9,8 @@
 // Deterministic: a fixed sequential fp32 sum per element, no atomics.
 //
 // One warp per (token, 256-column chunk), 8 tokens per CTA, grid.y = column
-// chunks (so a 64-token decode step still spreads over 64 CTAs): the warp ranks
+// chunks (so a 64-token decode step still spreads over 64 CTAs; at prefill sizes
+// grid.y shrinks and a warp takes several chunks): the warp ranks
 // the token's <= 32 slots by expert id with shuffles (no shared memory, no CTA
 // barrier), then each lane sums 8 columns with 16-byte loads of the per-pair
 // rows (fp32 on the decode path, bf16 on the prefill path: the sum stays fp32),
@@ -20,6 +21,7 @@
 namespace beam {
 
 constexpr int kCombineWarps = 8;
+constexpr int kCombineTargetCtas = 148 * 3 * 4;  // ~4 waves of 3 CTAs per SM (scaled to the SM count)
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   const uint32_t a = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
@@ -67,8 +69,10 @@ __global__ void __launch_bounds__(32 * kCombineWarps, 3) combine_kernel(const in
     const int pj = __shfl_sync(0xffffffffu, pos, j);
     if (pj >= 0 && rj == lane) sorted_pos = pj;
   }
-  {
-    const int c0 = blockIdx.y * 256 + 8 * lane;
+  // a warp walks column chunks blockIdx.y, +gridDim.y, ... with the same slot
+  // ranking (one slot_pos round trip for all of them)
+  for (int cy = blockIdx.y; cy * 256 < d; cy += gridDim.y) {
+    const int c0 = cy * 256 + 8 * lane;
     float y[8], hv[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) y[q] = 0.0f;
@@ -148,7 +152,13 @@ template <typename TP>
 static cudaError_t combine_dispatch(const PlanDev& p, const TP* opair, int T, int Keff, int d, int d_pad,
                                     const void* h, int h_dtype, void* out, int out_dtype, cudaStream_t s) {
   const bool vec = d % 8 == 0 && (reinterpret_cast<uintptr_t>(h) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  const dim3 grid(ceil_div(T, kCombineWarps), ceil_div(d, 256));
+  const int chunks = ceil_div(d, 256);
+  // enough chunk columns for ~4 waves of 3 CTAs per SM, no more: every extra
+  // column repeats the slot ranking and its dependent slot_pos load
+  // (T = 8192, d = 2048: 2 columns of 4 chunks, combine 77 -> 59 us)
+  const int tiles = ceil_div(T, kCombineWarps);
+  const int gy = std::max(1, std::min(chunks, ceil_div(kCombineTargetCtas * num_sms() / 148, tiles)));
+  const dim3 grid(tiles, gy);
   const int thr = 32 * kCombineWarps;
   if (out_dtype == BEAM_F32 && h_dtype == BEAM_F32)
     return launch_pdl(combine_kernel<float, float, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const float*)h, (float*)out, vec);
