@@ -325,7 +325,7 @@ cudaError_t launch_router(const void* X, int x_dtype, const float* norm_w, const
 // 3. Stand-alone top-K + softmax + mask (prefill / wide N): one warp per token.
 // ---------------------------------------------------------------------------
 template <typename TX, int NPL, int KIND>
-__global__ void __launch_bounds__(128) topk_mask_kernel(const float* __restrict__ L, int splits,
+__global__ void __launch_bounds__(128, NPL <= 4 ? 8 : 1) topk_mask_kernel(const float* __restrict__ L, int splits,
                                                         const TX* __restrict__ X, int T, TopkArgs a) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (t >= T) return;
