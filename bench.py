@@ -102,6 +102,15 @@ def calibrate_theta(h_bf16, router, mask, k: int, s: float) -> float:
     return float(0.5 * (r[r.size - m - 1] + r[r.size - m]))  # exactly m slots masked (away from ties)
 
 
+def workload_config(t: int, s: float) -> dict:
+    """The `config` object of BOTH arms (ours and --impl reference): the same
+    workload description, key for key; measurement details live elsewhere."""
+    return {"workload": f"Qwen3-30B-A3B MoE layer decode T={t} s={s} (configs[1])", "T": t,
+            "sparsity_target": s, **Q30, "routing_dtype": "f32", "expert_dtype": "bf16",
+            "tokens": "synthetic N(0,1), channel 0 = 8, bf16; mask row 0 = theta calibrated to s",
+            "parallelism": "single device"}
+
+
 def mask_with_theta(mask, theta: float):
     m = mask.clone()
     m[0] = theta
@@ -271,8 +280,8 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"Qwen3-30B-A3B MoE layer decode T={t} s={args.sparsity}",
-                   "T": t, "sparsity": args.sparsity, **Q30, "parallelism": "cpu"},
+        "config": workload_config(t, args.sparsity),
+        "measurement": {"where": "host CPU", "timing": "time.perf_counter over the steps"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "reference",
                          "sample": f"{args.steps} calls of beamoe.beam.beam_block_forward(training=False) "
                                    f"(numpy fp64 + Cython dispatch, {api} threads={cores}) on T={t}"},
@@ -617,6 +626,20 @@ def run_ours(args):
                               "hbm_frac_of_measured": round(byt / sec / 1e9 / hbm_peak, 4)})
                 del p
 
+    # ---- SPEC C9 / `beamoe bench-dispatch` defaults (cli.py:386-403): grouped
+    #      execution at active fractions 1.0 / 0.5 / 0.25, min over 20 reps --------
+    bench_dispatch = None
+    if not args.no_sweep:
+        rows = B.dispatch.bench_dispatch(num_tokens=4096, num_experts=8, top_k=4, d_h=256, d_ff=512,
+                                         active_fractions=[1.0, 0.5, 0.25], repetitions=20, seed=0)
+        bench_dispatch = {"config": "T=4096 N=8 K=4 d_h=256 d_ff=512 block 16 seed 0, fp32 tokens, bf16 experts "
+                                    "(reference test_acceptance.py:299-313 / cli.py:386-403)",
+                          "rows": [{"active_fraction": r.active_fraction, "slots_executed": r.slots_executed,
+                                    "us_min": round(r.wall_time_ns_min / 1e3, 2),
+                                    "us_mean": round(r.wall_time_ns_mean / 1e3, 2)} for r in rows],
+                          "strictly_decreasing": bool(rows[0].wall_time_ns_min > rows[1].wall_time_ns_min
+                                                      > rows[2].wall_time_ns_min)}
+
     # ---- the other BASELINE shapes (tiny fp32, OLMoE, Qwen3-235B) ------------------
     shapes = [] if args.no_shapes else run_shapes(B, args, flush, dev, hbm_peak, tc_peak_sus)
 
@@ -657,12 +680,10 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"Qwen3-30B-A3B MoE layer decode T={t} s={s} (configs[1])", "T": t,
-                   "sparsity_target": s, "sparsity_actual": round(pt["s_real"], 4), **Q30,
-                   "routing_dtype": "f32", "expert_dtype": "bf16", "E_act": pt["e_act"],
-                   "surviving_slots": pt["r"], "l2": "flushed (512 MiB memset) before every timed step, not timed",
-                   "timing": "CUDA events per step around a CUDA-graph replay of the public layer call",
-                   "parallelism": "single GPU"},
+        "config": workload_config(t, s),
+        "measurement": {"sparsity_actual": round(pt["s_real"], 4), "E_act": pt["e_act"],
+                        "surviving_slots": pt["r"], "l2": "flushed (512 MiB memset) before every timed step, not timed",
+                        "timing": "CUDA events per step around a CUDA-graph replay of the public layer call"},
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": t * d * 2,
                 "d2h_bytes_per_step": probe.nbytes,
                 "path": "paper_2605_14438_b200.beam_block_forward(pinned host h) -> host outputs"},
@@ -683,6 +704,7 @@ def run_ours(args):
         "gpu_launches_per_step": launches_per_step,
         "gpu_launches_counted_total": int(launches),
         "sweep": sweep,
+        "bench_dispatch": bench_dispatch,
         "shapes": shapes,
         "train_mask_router": train,
         "lm_greedy_decode": lm_line,
@@ -705,7 +727,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-shapes", action="store_true", help="skip the tiny / OLMoE / Qwen3-235B shape lines")
-    ap.add_argument("--expert-path", default="auto", choices=("auto", "simt", "tc", "tc1", "stream"),
+    ap.add_argument("--expert-path", default="auto", choices=("auto", "simt", "tc", "tc1"),
                     help="expert-stage kernels (diagnostics; default auto)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -160,6 +160,13 @@ int beam_moe_execute(const beam_layer_t* layer, const void* x, int x_dtype, int 
 int beam_mask_route(const int64_t* topk_ids, const void* a, int a_dtype, int T, int K, int N,
                     int64_t* out, beam_stream_t stream);
 
+/* moe.topk_select (moe.py:116-119): out[t, :] = argsort(-logits[t], stable)[:K]
+ * for logits [T, N] of dtype (BEAM_F32 or BEAM_F64) — value descending, ties to
+ * the lower index, -0.0 == +0.0, -inf after every finite value, NaN last
+ * (numpy's sort order). */
+int beam_topk_select(const void* logits, int dtype, int T, int N, int K, int64_t* out,
+                     beam_stream_t stream);
+
 /* dispatch.align_block (group_by_expert _kernels.pyx:37-66 + padding, __init__.py:106-119).
  * ids int64 [T, K] (entries outside [0, N) are ignored).  Outputs (int32):
  *   counts [N]; offsets [N+1] padded exclusive scan (offsets[N] = padded total);
@@ -169,7 +176,13 @@ int beam_mask_route(const int64_t* topk_ids, const void* a, int a_dtype, int T, 
  *   {num_active, padded_total, real_total, 0}. */
 int beam_group_by_expert(const int64_t* ids, int T, int K, int N, int block_size,
                          int32_t* counts, int32_t* offsets, int32_t* tokens, int32_t* slots,
-                         int32_t* active, int32_t* meta, beam_stream_t stream);
+                         int32_t* active, int32_t* meta, void* workspace, size_t workspace_bytes,
+                         beam_stream_t stream);
+/* Scratch for beam_group_by_expert: with at least this many ZERO-INITIALISED
+ * bytes (reusable across calls; the kernels leave it zeroed), T*K > 16384 runs
+ * the multi-CTA permute that beam_layer_forward uses at prefill sizes; with
+ * NULL / fewer bytes the single-CTA permute (same results, bit for bit). */
+size_t beam_group_by_expert_workspace_bytes(int T, int K, int N);
 
 /* dispatch.grouped_execute (__init__.py:129-157) on a plan from beam_group_by_expert.
  * x: [T, d_h] of x_dtype, weights_hat f32 [T, N] dense, y f32 [T, d_h].
@@ -243,10 +256,6 @@ int beam_profile_end(float* stage_ms, int* calls);
  *  last top-K tile done, permute done, last top-K tile start, permute start,
  *  token 0: partials summed, top-K selected, softmax done, outputs stored}. */
 int beam_trace_gate(unsigned long long* dev_buf);
-/* Phase timeline of the fused decode kernel: u64[64 + 12 * grid] (zeroed by the
- * caller); slot 64 + m * grid + cta = %globaltimer of CTA `cta` at mark m, slots
- * 24..63 = CTA 0 sub-step clocks; NULL disables. */
-int beam_trace_decode(unsigned long long* dev_buf);
 const char* beam_last_cuda_error(void);
 const char* beam_build_info(void);
 /* 1 if `p` is page-locked host memory the GPU can address at the same pointer

@@ -25,6 +25,10 @@ rm -rf "$OUT"
 mkdir -p "$OUT"
 python -m pip install --quiet --no-index --no-build-isolation --no-deps \
     --target "$OUT" "$TMP/pkg" >"$TMP/pip.log" 2>&1 || { cat "$TMP/pip.log" >&2; exit 1; }
+# the reference's own test files (not installed by pip) for the reference-side
+# backend integration test (tests/test_gpu_integration.py): build output only,
+# git-ignored like the rest of oracle/_ref
+cp -r "$SRC/tests" "$OUT/reference_tests"
 python - "$OUT" <<'PY'
 import sys
 sys.path.insert(0, sys.argv[1])

@@ -33,7 +33,9 @@ EXPORTS = (
     "beam_gate",
     "beam_moe_execute",
     "beam_mask_route",
+    "beam_topk_select",
     "beam_group_by_expert",
+    "beam_group_by_expert_workspace_bytes",
     "beam_grouped_execute",
     "beam_rms_norm",
     "beam_ste_backward",
@@ -45,7 +47,6 @@ EXPORTS = (
     "beam_profile_begin",
     "beam_profile_end",
     "beam_trace_gate",
-    "beam_trace_decode",
     "beam_last_cuda_error",
     "beam_build_info",
     "beam_host_mapped",
@@ -128,7 +129,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_gate": (I, [LP, P, I, I, OP, P, S, P]),
         "beam_moe_execute": (I, [LP, P, I, I, I, P, P, P, P, S, P]),
         "beam_mask_route": (I, [P, P, I, I, I, I, P, P]),
-        "beam_group_by_expert": (I, [P, I, I, I, I, P, P, P, P, P, P, P]),
+        "beam_topk_select": (I, [P, I, I, I, I, P, P]),
+        "beam_group_by_expert": (I, [P, I, I, I, I, P, P, P, P, P, P, P, S, P]),
+        "beam_group_by_expert_workspace_bytes": (S, [I, I, I]),
         "beam_grouped_execute": (I, [LP, P, I, I, I, I, P, P, P, P, P, P, P, P, P, P, S, P]),
         "beam_rms_norm": (I, [P, I, I, I, P, P, P]),
         "beam_ste_backward": (I, [P, P, P, I, I, I, ctypes.c_float, P, P]),
@@ -140,7 +143,6 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_profile_begin": (I, [I]),
         "beam_profile_end": (I, [P, P]),
         "beam_trace_gate": (I, [P]),
-        "beam_trace_decode": (I, [P]),
         "beam_last_cuda_error": (ctypes.c_char_p, []),
         "beam_build_info": (ctypes.c_char_p, []),
         "beam_host_mapped": (I, [P]),

@@ -9,6 +9,11 @@ import torch
 
 _lock = threading.Lock()
 _workspaces: dict = {}
+# Superseded workspaces stay alive: a CUDA graph captured while one of them was
+# current still points at it (and at its grid-completion counters), so freeing
+# it on growth would make a later replay a use-after-free.  Geometric growth
+# bounds what this keeps to ~2x the largest workspace per stream.
+_retired: list = []
 
 
 def stream_handle(device: torch.device) -> int:
@@ -31,11 +36,16 @@ def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
                               RuntimeWarning, stacklevel=3)
             # zero-filled once: the grid-completion counters at its start must
             # begin at 0 (the kernels reset them after every use)
+            if buf is not None:
+                _retired.append(buf)
             buf = torch.zeros(size, dtype=torch.uint8, device=device)
             _workspaces[key] = buf
         return buf
 
 
 def release_workspaces() -> None:
+    """Drop every cached workspace (only safe once no captured graph that used
+    one will be replayed again)."""
     with _lock:
         _workspaces.clear()
+        _retired.clear()

@@ -397,6 +397,6 @@ def set_expert_path(mode: str = "auto") -> None:
     grouped GEMM for prefill-sized batches, weight streaming for decode),
     "simt" (weight streaming always), "tc" (tcgen05 always, bf16 weights; 2-SM
     CTA pairs) or "tc1" (tcgen05 always, 1-SM kernel)."""
-    code = {"auto": 0, "simt": 1, "tc": 2, "tc1": 3, "stream": 4}[mode]
+    code = {"auto": 0, "simt": 1, "tc": 2, "tc1": 3}[mode]
     _lib.check(_lib.load().beam_set_expert_path(code), "beam_set_expert_path")
     _EXPERT_PATH[0] = code

@@ -325,18 +325,9 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
 
   prof_mark(0, s);
   BEAM_TRY(strided_input(g, h, h_dtype, T, w, &X, s));
-  if (sp.kind == BEAM_ROUTE_BEAM && !w.tc && g_expert_path.load() != 4 && decode_fused_supported(L, g, T)) {
-    // decode: the whole layer in one persistent kernel
-    BEAM_TRY(launch_decode_fused(L, g, X, h_dtype, T, topk_args(L, g, o, w, sp), w.logits2, w.act,
-                                 reinterpret_cast<unsigned*>(w.counters + 32), o->out, s));
-    if (o->decision_event) BEAM_TRY(cudaEventRecord(static_cast<cudaEvent_t>(o->decision_event), s));
-    for (int m = 1; m < kStageMarks; ++m) prof_mark(m, s);
-    return BEAM_OK;
-  }
   // decode with an RMS norm: the fused gate also writes x * norm_w (fp32) for the
   // weight-streaming expert kernels
-  const bool prescaled = L.has_norm && w.xw != nullptr && !w.tc && g_expert_path.load() != 4 &&
-                         gate_fused_supported(T, g.N, g.E, g.d_pad);
+  const bool prescaled = L.has_norm && w.xw != nullptr && !w.tc && gate_fused_supported(T, g.N, g.E, g.d_pad);
   if (gate_fused_supported(T, g.N, g.E, g.d_pad)) {
     // decode: projection + top-K + permute in one launch
     BEAM_TRY(launch_gate_fused(X, h_dtype, L.has_norm ? L.norm_w : nullptr, L.gate_wT, T, g.d, g.d_pad,
@@ -355,12 +346,6 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
                            w.plan, w.cap, w.xperm, s));
     BEAM_TRY(launch_experts_tc(L, g, w.xperm, w.plan, w.cap, w.act16, w.opair, s));
     prof_mark(3, s);
-    prof_mark(4, s);
-  } else if (g_expert_path.load() == 4 && stream_supported(L, g)) {  // bulk-copy streaming (experimental)
-    BEAM_TRY(launch_gateup_stream(L, g, X, h_dtype, L.has_norm ? w.inv : nullptr,
-                                  L.has_norm ? L.norm_w : nullptr, w.plan, w.act, s));
-    prof_mark(3, s);
-    BEAM_TRY(launch_down_stream(L, g, w.plan, w.act, w.opair, s));
     prof_mark(4, s);
   } else {
     if (prescaled)
@@ -448,9 +433,18 @@ int beam_mask_route(const int64_t* topk_ids, const void* a, int a_dtype, int T, 
                                   reinterpret_cast<cudaStream_t>(stream)));
 }
 
+int beam_topk_select(const void* logits, int dtype, int T, int N, int K, int64_t* out, beam_stream_t stream) {
+  if (T < 0 || N < 1 || K < 1 || K > N) return BEAM_ERR_ARG;
+  if (dtype != BEAM_F32 && dtype != BEAM_F64) return BEAM_ERR_ARG;
+  if (T == 0) return BEAM_OK;
+  if (!logits || !out) return BEAM_ERR_ARG;
+  return status(launch_topk_select(logits, dtype, T, N, K, out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int beam_group_by_expert(const int64_t* ids, int T, int K, int N, int block_size,
                          int32_t* counts, int32_t* offsets, int32_t* tokens, int32_t* slots,
-                         int32_t* active, int32_t* meta, beam_stream_t stream) {
+                         int32_t* active, int32_t* meta, void* workspace, size_t workspace_bytes,
+                         beam_stream_t stream) {
   if (T < 0 || K < 0 || N < 0 || block_size < 1) return BEAM_ERR_ARG;
   if (N > 1024) return BEAM_ERR_UNSUPPORTED;
   if (!offsets || !meta || (N > 0 && (!counts || !active))) return BEAM_ERR_ARG;
@@ -462,8 +456,14 @@ int beam_group_by_expert(const int64_t* ids, int T, int K, int N, int block_size
   p.meta = meta;
   p.tok = tokens;
   p.slot = slots;
-  return status(launch_permute<int64_t>(ids, nullptr, T, K, N, block_size, p, nullptr,
+  int* scratch = (workspace && workspace_bytes >= permute_scratch_bytes(T, K, N)) ? static_cast<int*>(workspace) : nullptr;
+  return status(launch_permute<int64_t>(ids, nullptr, T, K, N, block_size, p, scratch,
                                         reinterpret_cast<cudaStream_t>(stream)));
+}
+
+size_t beam_group_by_expert_workspace_bytes(int T, int K, int N) {
+  if (T < 0 || K < 0 || N < 0) return 0;
+  return permute_scratch_bytes(T, K, N);
 }
 
 int beam_grouped_execute(const beam_layer_t* layer, const void* x, int x_dtype, int T, int K,
@@ -581,7 +581,7 @@ int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w,
 unsigned long long beam_kernel_launches(void) { return g_launches.load(); }
 
 int beam_set_expert_path(int mode) {
-  if (mode < 0 || mode > 4) return BEAM_ERR_ARG;
+  if (mode < 0 || mode > 3) return BEAM_ERR_ARG;
   g_expert_path.store(mode == 3 ? 2 : mode);
   set_gemm_variant(mode == 3 ? 1 : 0);
   return BEAM_OK;
@@ -620,8 +620,6 @@ int beam_profile_end(float* stage_ms, int* calls) {
 }
 
 int beam_trace_gate(unsigned long long* dev_buf) { return status(beam::set_gate_trace(dev_buf)); }
-
-int beam_trace_decode(unsigned long long* dev_buf) { return status(beam::set_decode_trace(dev_buf)); }
 
 const char* beam_last_cuda_error(void) { return g_last_error; }
 

@@ -113,6 +113,7 @@ cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, c
                               float* xw = nullptr);  // xw: [T, d_pad] x * norm_w (fp32) when norm_w is set
 cudaError_t launch_mask_route(const int64_t* ids, const void* a, int a_dtype, int T, int K,
                               int N, int64_t* out, cudaStream_t s);
+cudaError_t launch_topk_select(const void* logits, int dtype, int T, int N, int K, int64_t* out, cudaStream_t s);
 
 // permute.cu
 // scratch: permute_scratch_bytes() bytes, zero-initialised once (multi-CTA path
@@ -134,32 +135,13 @@ cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void*
                                cudaStream_t s, long long slots = -1);
 cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const PlanDev& p,
                              const float* act, float* opair, cudaStream_t s, long long slots = -1);
-// experts_stream.cu (bulk-copy weight streaming, bf16 weights)
-bool stream_supported(const beam_layer_t& L, const Dims& g);
-cudaError_t launch_gateup_stream(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype,
-                                 const float* inv, const float* nw, const PlanDev& p, float* act, cudaStream_t s);
-cudaError_t launch_down_stream(const beam_layer_t& L, const Dims& g, const PlanDev& p, const float* act,
-                               float* opair, cudaStream_t s);
-
-// Decode expert stage: bulk-copy streaming for bf16 weights, SIMT loads otherwise.
-inline cudaError_t launch_experts_decode(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
-                                         const float* inv, const float* nw, const PlanDev& p, float* act,
-                                         float* opair, cudaStream_t s) {
-  cudaError_t e;
-  if (false && stream_supported(L, g)) {  // the bulk-copy kernels are still slower than the SIMT stream
-    e = launch_gateup_stream(L, g, X, x_dtype, inv, nw, p, act, s);
-    if (e != cudaSuccess) return e;
-    return launch_down_stream(L, g, p, act, opair, s);
-  }
-  e = launch_gateup_simt(L, g, X, x_dtype, T, inv, nw, p, act, s);
-  if (e != cudaSuccess) return e;
-  return launch_down_simt(L, g, T, p, act, opair, s);
-}
-
+// Decode expert stage on externally routed rows (no norm): gate/up then down.
 inline cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, const void* X,
                                        int x_dtype, int T, const PlanDev& p, float* act, float* opair,
                                        cudaStream_t s) {
-  return launch_experts_decode(L, g, X, x_dtype, T, nullptr, nullptr, p, act, opair, s);
+  cudaError_t e = launch_gateup_simt(L, g, X, x_dtype, T, nullptr, nullptr, p, act, s);
+  if (e != cudaSuccess) return e;
+  return launch_down_simt(L, g, T, p, act, opair, s);
 }
 
 // experts_tc.cu (tcgen05 grouped GEMM, prefill)
@@ -176,12 +158,6 @@ cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* ga
 // opair written as bf16 [cap, d_pad] (combine reads it with BEAM_BF16)
 cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* xperm, const PlanDev& p,
                               int cap, void* act16, void* opair, cudaStream_t s);
-
-// decode_fused.cu (whole layer, T <= 64, one persistent cooperative kernel)
-bool decode_fused_supported(const beam_layer_t& L, const Dims& g, int T);
-cudaError_t launch_decode_fused(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
-                                const TopkArgs& tk, float* P, void* act, unsigned* bar, void* out,
-                                cudaStream_t s);
 
 // combine.cu
 cudaError_t launch_combine(const PlanDev& p, const void* opair, int opair_dtype, int T, int Keff, int d, int d_pad,
@@ -205,6 +181,5 @@ cudaError_t launch_trace_rows(const int64_t* topk, const int64_t* masked, const 
                               int64_t* rows, unsigned long long* active, cudaStream_t s);
 
 cudaError_t set_gate_trace(unsigned long long* buf);
-cudaError_t set_decode_trace(unsigned long long* buf);
 
 }  // namespace beam

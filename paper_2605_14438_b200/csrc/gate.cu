@@ -283,9 +283,14 @@ static int gemv_kr(int T, int cols, int d_pad, int max_split, int tt = kGemvTT) 
   return ceil_div(ceil_div(d_pad, s), kGemvK) * kGemvK;
 }
 
+// The decode projection writes at most kRouterMaxSplit split-K partials: the
+// workspace holds that many [T][cols] slabs (abi.cu carve) and the top-K kernel
+// sums at most that many.  kr <= kGemvSteps * kGemvK = 1024 covers d_pad <= 16384.
+constexpr int kRouterMaxSplit = 16;
+
 int router_splits(int T, int cols, int d_pad) {
   if (T > 64) return 1;
-  return ceil_div(d_pad, gemv_kr(T, cols, d_pad, 1 << 20));
+  return ceil_div(d_pad, gemv_kr(T, cols, d_pad, kRouterMaxSplit));
 }
 
 template <typename K>
@@ -297,8 +302,9 @@ cudaError_t launch_router(const void* X, int x_dtype, const float* norm_w, const
                           int T, int cols, int d, int d_pad, float* P, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (T <= 64) {
-    const int kr = gemv_kr(T, cols, d_pad, 1 << 20);
+    const int kr = gemv_kr(T, cols, d_pad, kRouterMaxSplit);
     dim3 grid(ceil_div(cols, 8 * kGemvCols), ceil_div(d_pad, kr), ceil_div(T, kGemvTT));
+    if ((int)grid.y > kRouterMaxSplit) return cudaErrorInvalidValue;  // d_pad > 16384: before any launch
     const size_t smem = (size_t)kGemvTT * kr * sizeof(float);
     static bool attr = false;
     if (!attr) {
@@ -354,7 +360,7 @@ static void topk_dispatch(const float* L, int splits, const void* X, int T, cons
 cudaError_t launch_topk_mask(const float* L, int splits, const void* X, int x_dtype, int T,
                              const TopkArgs& a, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
-  if (splits > 16) return cudaErrorInvalidValue;
+  if (splits > kRouterMaxSplit) return cudaErrorInvalidValue;
   if (x_dtype == BEAM_BF16) topk_dispatch<__nv_bfloat16>(L, splits, X, T, a, s);
   else topk_dispatch<float>(L, splits, X, T, a, s);
   count_launches(1);
@@ -530,6 +536,67 @@ cudaError_t launch_mask_route(const int64_t* ids, const void* a, int a_dtype, in
     mask_route_kernel<double><<<grid, 256, 0, s>>>(ids, (const double*)a, T, K, N, out);
   else
     mask_route_kernel<float><<<grid, 256, 0, s>>>(ids, (const float*)a, T, K, N, out);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// 5. Stand-alone topk_select (moe.py:116-119): argsort(-logits, stable)[:k] on
+//    arbitrary fp32 / fp64 logits.  One warp per row; round r picks the best
+//    entry strictly below round r-1's pick in the total order (value desc, ties
+//    -> lower index), so no per-entry state is kept for any N.  numpy's order:
+//    -0.0 == +0.0 (stable), +inf first, -inf after every finite value, NaN last.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long order_key(double x) {
+  if (x != x) return 0ull;  // NaN: last
+  if (x == 0.0) x = 0.0;    // -0.0 ties with +0.0 (stable sort keeps index order)
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // >= 1 for every non-NaN value
+}
+
+template <typename TL>
+__global__ void __launch_bounds__(256) topk_select_kernel(const TL* __restrict__ L, int T, int N, int K,
+                                                          int64_t* __restrict__ out) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const TL* r = L + (size_t)row * N;
+  unsigned long long lk = ~0ull;  // previous pick (key, index); the first round has no bound
+  int lj = -1;
+  for (int k = 0; k < K; ++k) {
+    unsigned long long bk = 0ull;
+    int bj = 0x7fffffff;
+    for (int j = lane; j < N; j += 32) {
+      const unsigned long long key = order_key((double)r[j]);
+      const bool below = k == 0 || key < lk || (key == lk && j > lj);
+      const bool better = key > bk || (key == bk && j < bj);
+      if (below && better) {
+        bk = key;
+        bj = j;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ok > bk || (ok == bk && oj < bj)) {
+        bk = ok;
+        bj = oj;
+      }
+    }
+    if (lane == 0) out[(size_t)row * K + k] = bj;
+    lk = bk;
+    lj = bj;
+  }
+}
+
+cudaError_t launch_topk_select(const void* logits, int dtype, int T, int N, int K, int64_t* out, cudaStream_t s) {
+  if (T <= 0 || K <= 0) return cudaSuccess;
+  const int grid = ceil_div(T, 8);
+  if (dtype == BEAM_F64)
+    topk_select_kernel<double><<<grid, 256, 0, s>>>((const double*)logits, T, N, K, out);
+  else
+    topk_select_kernel<float><<<grid, 256, 0, s>>>((const float*)logits, T, N, K, out);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -430,11 +430,19 @@ def topk_route(x, router_weights, k: int) -> RouterDecision:
 
 def topk_select(logits, k: int) -> torch.Tensor:
     """moe.py:116-119: indices of the k largest entries per row, ties won by the
-    lower index (identity router through the gating kernel; exact in fp32)."""
+    lower index (numpy's stable argsort order on -logits: NaN last, -0.0 == +0.0).
+    fp64 logits are compared in fp64 (``beam_topk_select``, one warp per row)."""
     lg = as_torch(logits)
     n = lg.shape[-1]
     if not 1 <= k <= n:
         raise ContractError("top_k must satisfy 1 <= K <= N")
     dev = lg.device if lg.is_cuda else _default_device()
-    eye = torch.eye(n, dtype=torch.float32, device=dev)
-    return _gate_call(lg, eye, None, k, want=("topk_ids",))["topk_ids"]
+    dt = torch.float64 if lg.dtype == torch.float64 else torch.float32
+    x = lg.to(dev, dt).contiguous()
+    lead = x.shape[:-1]
+    x = x.reshape(-1, n)
+    out = torch.empty(x.shape[0], k, dtype=torch.int64, device=dev)
+    _lib.check(_lib.load().beam_topk_select(x.data_ptr(), _lib.BEAM_F64 if dt == torch.float64 else _lib.BEAM_F32,
+                                            x.shape[0], n, k, out.data_ptr(), _runtime.stream_handle(dev)),
+               "beam_topk_select")
+    return out.reshape(*lead, k)

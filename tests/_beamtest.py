@@ -56,9 +56,19 @@ def topk_margin_ok(logits: np.ndarray, k: int, tol: float) -> np.ndarray:
     return ok
 
 
+def assert_kept(ok: np.ndarray, floor: float = 0.9) -> None:
+    """Tests that exclude near-tie tokens from an exact comparison must still
+    compare most of them: a floor on the kept fraction (and at least one token),
+    so an all-excluded case cannot pass vacuously."""
+    assert ok.size > 0 and ok.any(), "every token excluded as a near tie"
+    assert ok.mean() > floor, f"only {ok.mean():.3f} of the tokens kept (floor {floor})"
+
+
 def normwise_rel(a: np.ndarray, b: np.ndarray) -> float:
-    """max |a - b| / max |b| (the 'max rel err' of the north-star tolerance)."""
-    den = float(np.max(np.abs(b))) if b.size else 0.0
+    """max |a - b| / max |b| (the 'max rel err' of the north-star tolerance).
+    Empty inputs are an error (a comparison of nothing must not pass)."""
+    assert b.size > 0, "normwise_rel on an empty selection"
+    den = float(np.max(np.abs(b)))
     return float(np.max(np.abs(a - b))) / den if den > 0 else float(np.max(np.abs(a - b), initial=0.0))
 
 

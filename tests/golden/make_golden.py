@@ -30,6 +30,13 @@ lm                — trainer.TinyMoELM (trainer.py:150-257) with BEAM routing a
 q30route_dyadic   — Qwen3-30B-A3B router shape (N=128, K=8, d=2048), dyadic inputs,
                     so logits / pre-activations are exact in fp32 and fp64: top-K ids,
                     mask bits and the plan must match bit-for-bit.
+q30prefill_dyadic — the same at the PREFILL size (configs[2], T=8192): bf16-exact
+                    dyadic tokens h = hq/8 regenerated from a seed (sha256-checked),
+                    router / mask weights j/256 — routes through the tensor-core
+                    router, the top-K kernel and the multi-CTA permute; ids, mask
+                    bits, masked ids and the block-16 plan are stored (compactly).
+
+    python tests/golden/make_golden.py [name ...]    # default: every fixture
 """
 
 from __future__ import annotations
@@ -259,6 +266,54 @@ def make_lm():
          avg_k=np.float64(ev.avg_k), token_count=np.int64(ev.token_count), trace_csv=csv_bytes)
 
 
+Q30_PREFILL_SEED = 8192
+
+
+def q30prefill_tokens(seed: int = Q30_PREFILL_SEED, t: int = 8192, d: int = 2048) -> np.ndarray:
+    """hq (int8, h = hq / 8) of the q30prefill_dyadic fixture (numpy PCG64; the
+    fixture stores its sha256 so a changed generator is detected, not trusted)."""
+    return np.random.default_rng(seed).integers(-16, 17, (t, d)).astype(np.int8)
+
+
+def make_q30prefill_dyadic():
+    """Routing half of beam_block_forward (moe.py:122-137, beam.py:68-72,
+    dispatch/__init__.py:55-62, 89-126) at T = 8192 on dyadic inputs."""
+    import hashlib
+
+    ref.import_beamoe()
+    from beamoe import dispatch
+    from beamoe.beam import MaskRouter, mask_forward
+    from beamoe.moe import topk_route
+    from beamoe.tensor import Tensor
+
+    d, n, k, t = 2048, 128, 8, 8192
+    hq = q30prefill_tokens()
+    rng = np.random.default_rng(Q30_PREFILL_SEED + 1)
+    rq = rng.integers(-32, 33, (d, n)).astype(np.int8)          # router = rq / 256
+    rq[:, 100:104] = rq[:, 96:100]                              # duplicated columns: exact logit ties
+    mq = rng.integers(-32, 33, (d, n)).astype(np.int8)          # mask_w = mq / 256
+    mq[:, :4] = 0                                               # a == 0 exactly: inclusive boundary
+    x = Tensor(hq.astype(np.float64) / 8.0)
+    dec = topk_route(x, Tensor(rq.astype(np.float64) / 256.0), k)
+    mdec = mask_forward(x, MaskRouter(Tensor(mq.astype(np.float64) / 256.0)))
+    masked_ids = dispatch.mask_route(dec.topk_indices, mdec.pre_activation.data)
+    plan = dispatch.align_block(masked_ids, 16, num_experts=n)
+    pa = _plan_arrays(plan)
+    logits = np.ascontiguousarray(dec.logits.data)
+    pre = np.ascontiguousarray(mdec.pre_activation.data)
+    save("q30prefill_dyadic",
+         seed=np.int64(Q30_PREFILL_SEED), hq_sha256=np.array(hashlib.sha256(hq.tobytes()).hexdigest()),
+         rq=rq, mq=mq,
+         logits_sha256=np.array(hashlib.sha256(logits.tobytes()).hexdigest()),
+         pre_activation_sha256=np.array(hashlib.sha256(pre.tobytes()).hexdigest()),
+         topk_ids=dec.topk_indices.astype(np.uint8),
+         mask_bits=np.packbits(mdec.mask.data.astype(np.uint8), axis=1),
+         masked_ids=masked_ids.astype(np.int16),
+         weights_topk=np.take_along_axis(dec.weights.data, dec.topk_indices, 1),
+         plan_counts=pa["plan_counts"].astype(np.int32), plan_offsets=pa["plan_offsets"].astype(np.int32),
+         plan_tokens=pa["plan_tokens"].astype(np.int16), plan_slots=pa["plan_slots"].astype(np.int8))
+
+
 def main():
     make_lm()
     make_trace()
@@ -410,4 +465,9 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"make_{name}"]()
+    else:
+        main()
+        make_q30prefill_dyadic()

@@ -18,7 +18,7 @@ if not torch.cuda.is_available():  # the gpu marker is deselected on CPU runs
 import paper_2605_14438_b200 as B  # noqa: E402
 from paper_2605_14438_b200 import dispatch as D  # noqa: E402
 from oracle import beam_oracle as O  # noqa: E402
-from _beamtest import golden_block, mask_margin_ok, matched_blocks, normwise_rel, topk_margin_ok  # noqa: E402
+from _beamtest import assert_kept, golden_block, mask_margin_ok, matched_blocks, normwise_rel, topk_margin_ok  # noqa: E402
 
 TOL_BF16 = 1e-2
 TOL_F32 = 1e-4
@@ -133,6 +133,66 @@ def test_q30_routing_dyadic_bit_exact(golden):
     assert np.array_equal(_np(plan.flat_slots[: offs[-1]]).astype(np.int64), g["plan_slots"])
 
 
+def test_q30_prefill_dyadic_bit_exact(golden):
+    """configs[2] prefill size, T = 8192, through the AUTO path of the public layer
+    call (tensor-core 3-split router, top-K kernel, multi-CTA permute, tcgen05
+    grouped GEMMs): on dyadic bf16 tokens the fp32 logits and mask pre-activations
+    are exact, so they, the top-K ids (with exact ties from duplicated router
+    columns), the mask bits, the masked ids and the block-16 plan must equal the
+    REFERENCE's (tests/golden/q30prefill_dyadic.npz, make_golden.py) bit for bit;
+    every token's output is checked against the fp64 oracle (1024-token chunks)."""
+    import hashlib
+
+    g = golden("q30prefill_dyadic")
+    hq = np.random.default_rng(int(g["seed"])).integers(-16, 17, (8192, 2048)).astype(np.int8)
+    assert hashlib.sha256(hq.tobytes()).hexdigest() == str(g["hq_sha256"]), "token generator changed"
+    d, f, n, k, t = 2048, 768, 128, 8, 8192
+    router, mask_w = g["rq"].astype(np.float64) / 256, g["mq"].astype(np.float64) / 256
+    gen = torch.Generator().manual_seed(2605)
+    wg = torch.empty(n, d, f).normal_(0, 0.02, generator=gen).to(torch.bfloat16)
+    wu = torch.empty(n, d, f).normal_(0, 0.02, generator=gen).to(torch.bfloat16)
+    wd = torch.empty(n, f, d).normal_(0, 0.02, generator=gen).to(torch.bfloat16)
+    cfg = B.MoEBlockConfig(d_h=d, d_ff=f, num_experts=n, top_k=k, has_norm=False)
+    gb = B.MoEBlock.from_weights(cfg, router, (wg, wu, wd), mask_w=mask_w)
+    x = torch.from_numpy(hq).to(torch.bfloat16).cuda() / 8  # exact in bf16
+    out, dec, md = B.beam_block_forward(x, gb, training=False)
+    # the in-layer masked ids (same C-ABI call, outputs carved by the wrapper)
+    outs = B.beam.LayerOutputs(t, d, n, k, torch.bfloat16, x.device)
+    B.beam.layer_forward_into(x, gb, outs)
+    torch.cuda.synchronize()
+    logits = np.ascontiguousarray(_np(dec.logits).astype(np.float64))
+    pre = np.ascontiguousarray(_np(md.pre_activation).astype(np.float64))
+    assert hashlib.sha256(logits.tobytes()).hexdigest() == str(g["logits_sha256"])
+    assert hashlib.sha256(pre.tobytes()).hexdigest() == str(g["pre_activation_sha256"])
+    ids = _np(dec.topk_indices)
+    assert np.array_equal(ids, g["topk_ids"].astype(np.int64))
+    assert np.array_equal(np.packbits(_np(md.mask).astype(np.uint8), axis=1), g["mask_bits"])
+    masked = outs["masked_ids"]
+    assert np.array_equal(_np(masked), g["masked_ids"].astype(np.int64))
+    assert torch.equal(outs["out"], out)  # deterministic across calls
+    np.testing.assert_allclose(np.take_along_axis(_np(dec.weights), ids, 1), g["weights_topk"], rtol=0, atol=1e-6)
+    plan = D.align_block(masked, 16, n)  # T*K = 65536 slots: the multi-CTA permute
+    offs = _np(plan.offsets).astype(np.int64)
+    assert np.array_equal(offs, g["plan_offsets"].astype(np.int64))
+    assert np.array_equal(_np(plan.real_counts).astype(np.int64), g["plan_counts"].astype(np.int64))
+    assert np.array_equal(_np(plan.flat_tokens[: offs[-1]]).astype(np.int64), g["plan_tokens"].astype(np.int64))
+    assert np.array_equal(_np(plan.flat_slots[: offs[-1]]).astype(np.int64), g["plan_slots"].astype(np.int64))
+    # outputs: every token vs the oracle on the same (dequantised bf16) weights
+    ob = O.OracleBlock(d_h=d, d_ff=f, num_experts=n, top_k=k, router_w=router,
+                       experts=[(wg[e].double().numpy(), wu[e].double().numpy(), wd[e].double().numpy())
+                                for e in range(n)],
+                       shared=[], norm_w=None, mask_w=mask_w)
+    o_all = _np(out.float()).astype(np.float64)
+    h64 = hq.astype(np.float64) / 8
+    worst = 0.0
+    for c0 in range(0, t, 1024):
+        sub = slice(c0, c0 + 1024)
+        ref = O.beam_block_forward(h64[sub], ob)
+        assert np.array_equal(ids[sub], ref.decision.topk_indices)
+        worst = max(worst, normwise_rel(o_all[sub], ref.out))
+    assert worst <= TOL_BF16, worst
+
+
 # ---------------------------------------------------------------------------
 # full layer vs oracle at the north-star shapes
 # ---------------------------------------------------------------------------
@@ -159,6 +219,7 @@ def test_layer_q30_decode_bf16(t, mask_std):
                                                  h_dtype=torch.bfloat16)
     ok = topk_margin_ok(ref.decision.logits, 8, 1e-5)
     ok &= mask_margin_ok(ref, 1e-5)
+    assert_kept(ok)
     assert np.array_equal(_np(dec.topk_indices)[ok], ref.decision.topk_indices[ok])
     assert np.array_equal(_np(md.mask)[ok], ref.mask.mask[ok])
     o = _np(out.float()).astype(np.float64)
@@ -174,6 +235,7 @@ def test_layer_q30_fp32_input_update():
     ob, gb, h64, ref, out, dec, md = _layer_case(2048, 768, 128, 8, 32, 7, 1 / np.sqrt(2048), "bf16")
     ok = topk_margin_ok(ref.decision.logits, 8, 1e-5)
     ok &= mask_margin_ok(ref, 1e-5)
+    assert_kept(ok)
     y = _np(out).astype(np.float64) - h64
     assert normwise_rel(y[ok], ref.y[ok]) <= TOL_BF16
 
@@ -196,6 +258,7 @@ def test_layer_tiny_fp32():
 def test_layer_shared_and_block_sizes(bs):
     ob, gb, h64, ref, out, dec, md = _layer_case(64, 48, 16, 4, 37, 50 + bs, 0.3, "f32", shared=2, bs=bs)
     ok = topk_margin_ok(ref.decision.logits, 4, 1e-5)
+    assert_kept(ok)
     o = _np(out).astype(np.float64)
     assert normwise_rel(o[ok], ref.out[ok]) <= TOL_F32
 
@@ -204,6 +267,7 @@ def test_layer_identity_activation_and_odd_dims():
     ob, gb, h64, ref, out, dec, md = _layer_case(37, 21, 5, 3, 11, 9, 0.5, "f32", activation="identity",
                                                  has_norm=False)
     ok = topk_margin_ok(ref.decision.logits, 3, 1e-5)
+    assert_kept(ok)
     assert normwise_rel(_np(out).astype(np.float64)[ok], ref.out[ok]) <= TOL_F32
 
 
@@ -275,6 +339,25 @@ def test_mask_forward_kats():
     assert _np(md.binary_mask).tolist() == [[0, 1]]
     md = B.mask_forward(torch.tensor([[0.0]]).cuda(), B.MaskRouter(torch.eye(1).cuda()))
     assert float(md.raw_mask[0, 0]) == 0.5 and int(md.binary_mask[0, 0]) == 1
+
+
+def test_topk_select_numpy_order():
+    """moe.topk_select (moe.py:116-119) == np.argsort(-x, stable)[:, :k] in fp32 and
+    fp64, with heavy ties, +-0, +-inf and NaN (numpy's sort order: NaN last)."""
+    rng = np.random.default_rng(116)
+    for dt in (np.float32, np.float64):
+        x = rng.integers(-3, 4, (300, 37)).astype(dt)
+        x[rng.random(x.shape) < 0.05] = np.nan
+        x[rng.random(x.shape) < 0.05] = np.inf
+        x[rng.random(x.shape) < 0.05] = -np.inf
+        x[rng.random(x.shape) < 0.1] = -0.0
+        x[0] = np.nan
+        x[1] = -np.inf
+        for k in (1, 5, 37):
+            ids = B.topk_select(torch.from_numpy(x).cuda(), k)
+            assert np.array_equal(_np(ids), np.argsort(-x, axis=-1, kind="stable")[:, :k]), (dt, k)
+    y = rng.normal(size=(4, 6, 130))  # leading dims are kept
+    assert np.array_equal(_np(B.topk_select(torch.from_numpy(y), 8)), np.argsort(-y, axis=-1, kind="stable")[..., :8])
 
 
 def test_rms_norm_matches_oracle():
@@ -380,6 +463,20 @@ def test_align_block_large_prefill_shape():
         assert np.array_equal(_np(plan.flat_slots[: offs[-1]]).astype(np.int64), np.concatenate(ref.slots))
 
 
+def test_spec_c9_bench_dispatch_ordering():
+    """SPEC criterion 9 (reference tests/test_acceptance.py:299-313, defaults of
+    `beamoe bench-dispatch`, cli.py:386-403): T=4096, N=8, K=4, d=256, f=512 —
+    executed slots within 2 % of the target and the min time strictly decreasing
+    over active fractions 1.0 > 0.5 > 0.25 (masked slots cost nothing)."""
+    rows = D.bench_dispatch(num_tokens=4096, num_experts=8, top_k=4, d_h=256, d_ff=512,
+                            active_fractions=[1.0, 0.5, 0.25], repetitions=20, seed=0)
+    total = 4096 * 4
+    for row in rows:
+        assert abs(row.slots_executed - row.active_fraction * total) <= 0.02 * total
+    assert rows[0].wall_time_ns_min > rows[1].wall_time_ns_min > rows[2].wall_time_ns_min, \
+        [r.wall_time_ns_min for r in rows]
+
+
 def test_bench_dispatch_slot_counts():
     rows = D.bench_dispatch(32, 4, 2, 8, 8, [1.0, 0.5], 2, seed=0)
     assert rows[0].slots_executed == 64
@@ -405,6 +502,7 @@ def test_layer_q30_tcgen05_path(tc_path, t, mask_std):
     ob, gb, h64, ref, out, dec, md = _layer_case(2048, 768, 128, 8, t, 500 + t, mask_std, "bf16",
                                                  h_dtype=torch.bfloat16)
     ok = topk_margin_ok(ref.decision.logits, 8, 1e-5) & mask_margin_ok(ref, 1e-5)
+    assert_kept(ok)
     assert np.array_equal(_np(dec.topk_indices)[ok], ref.decision.topk_indices[ok])
     o = _np(out.float()).astype(np.float64)
     assert normwise_rel(o[ok], ref.out[ok]) <= TOL_BF16
@@ -428,9 +526,10 @@ def test_tcgen05_matches_weight_streaming(tc_path):
 
 
 def test_prefill_auto_path_q30_8192():
-    """Q30 prefill (T=8192) through the auto path (tcgen05): finite, deterministic,
-    routing bit-identical to a decode-path run of the same tokens; a token subset
-    checked against the oracle."""
+    """Q30 prefill (T=8192) through the auto path (tensor-core router, top-K
+    kernel, multi-CTA permute, tcgen05 grouped GEMMs): deterministic, and EVERY
+    token checked against the fp64 oracle (in 1024-token chunks) — ids and mask
+    bits exact outside near ties, outputs within the bf16 tolerance."""
     rng = np.random.default_rng(8192)
     ob = O.make_block(2048, 768, 128, 8, rng, init_std=0.02)
     ob.mask_w = rng.normal(0, 1 / np.sqrt(2048), (2048, 128))
@@ -440,13 +539,19 @@ def test_prefill_auto_path_q30_8192():
     out, dec, md = B.beam_block_forward(x, gb, training=False)
     out2, _, _ = B.beam_block_forward(x, gb, training=False)
     assert torch.equal(out, out2)
-    assert torch.isfinite(out.float()).all()
-    sub = slice(0, 64)
-    ref = O.beam_block_forward(h[sub].double().numpy(), ob)
-    ok = topk_margin_ok(ref.decision.logits, 8, 1e-5) & mask_margin_ok(ref, 1e-5)
-    assert np.array_equal(_np(dec.topk_indices[sub])[ok], ref.decision.topk_indices[ok])
-    o = _np(out[sub].float()).astype(np.float64)
-    assert normwise_rel(o[ok], ref.out[ok]) <= TOL_BF16
+    ids, mask, o_all = _np(dec.topk_indices), _np(md.mask), _np(out.float()).astype(np.float64)
+    h64 = h.double().numpy()
+    kept, worst = [], 0.0
+    for c0 in range(0, 8192, 1024):
+        sub = slice(c0, c0 + 1024)
+        ref = O.beam_block_forward(h64[sub], ob)
+        ok = topk_margin_ok(ref.decision.logits, 8, 1e-5) & mask_margin_ok(ref, 1e-5)
+        kept.append(ok)
+        assert np.array_equal(ids[sub][ok], ref.decision.topk_indices[ok]), c0
+        assert np.array_equal(mask[sub][ok], ref.mask.mask[ok]), c0
+        worst = max(worst, normwise_rel(o_all[sub][ok], ref.out[ok]))
+    assert_kept(np.concatenate(kept))
+    assert worst <= TOL_BF16, worst
 
 
 def test_tcgen05_pair_matches_single_sm():
@@ -468,4 +573,5 @@ def test_tcgen05_pair_matches_single_sm():
     assert normwise_rel(y2, y1) <= 1e-2
     ref = O.beam_block_forward(x.double().cpu().numpy(), ob)
     ok = topk_margin_ok(ref.decision.logits, 8, 1e-5) & mask_margin_ok(ref, 1e-5)
+    assert_kept(ok)
     assert normwise_rel(_np(o2.float()).astype(np.float64)[ok], ref.out[ok]) <= TOL_BF16

@@ -213,3 +213,28 @@ def test_lm_init_matches_reference_draws():
             assert np.array_equal(a[w].numpy(), f32(b[w].data))
         assert np.array_equal(a["block"].router_w.numpy(), f32(b["block"].router_w.data))
     del torch
+
+
+def test_q30_prefill_dyadic_golden(golden):
+    """The oracle's routing half at the prefill size (T=8192, dyadic inputs)
+    reproduces the reference's fixture bit for bit (logit / pre-activation
+    hashes, ids, mask bits, masked ids, block-16 plan)."""
+    import hashlib
+
+    g = golden("q30prefill_dyadic")
+    hq = np.random.default_rng(int(g["seed"])).integers(-16, 17, (8192, 2048)).astype(np.int8)
+    assert hashlib.sha256(hq.tobytes()).hexdigest() == str(g["hq_sha256"])
+    x = hq.astype(np.float64) / 8
+    dec = O.topk_route(x, g["rq"].astype(np.float64) / 256, 8)
+    md = O.mask_forward(x, g["mq"].astype(np.float64) / 256)
+    assert hashlib.sha256(np.ascontiguousarray(dec.logits).tobytes()).hexdigest() == str(g["logits_sha256"])
+    assert hashlib.sha256(np.ascontiguousarray(md.pre_activation).tobytes()).hexdigest() == str(
+        g["pre_activation_sha256"])
+    assert np.array_equal(dec.topk_indices, g["topk_ids"].astype(np.int64))
+    assert np.array_equal(np.packbits(md.mask.astype(np.uint8), axis=1), g["mask_bits"])
+    masked = O.mask_route(dec.topk_indices, md.pre_activation)
+    assert np.array_equal(masked, g["masked_ids"].astype(np.int64))
+    offs, toks, slots = _plan_flat(O.align_block(masked, 16, 128))
+    assert np.array_equal(offs, g["plan_offsets"].astype(np.int64))
+    assert np.array_equal(toks, g["plan_tokens"].astype(np.int64))
+    assert np.array_equal(slots, g["plan_slots"].astype(np.int64))
