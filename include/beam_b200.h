@@ -250,6 +250,33 @@ unsigned long long beam_kernel_launches(void);
 int beam_set_expert_path(int mode);
 int beam_profile_begin(int max_calls);
 int beam_profile_end(float* stage_ms, int* calls);
+/* ---- expert parallelism (paper_2605_14438_b200/ep.py; not in the reference,
+ * whose PAPER.md:712 lists EP as open).  Rank r of `world` owns experts
+ * [r*N/world, (r+1)*N/world).  A send row per (token, destination rank) with at
+ * least one surviving slot there (deduplicated); x row = the token's raw h row,
+ * meta row = int32[2K+1]: K local ids (-1 = not this rank's / masked) | K ghat
+ * (f32 bits) | inv_rms (f32 bits).  FIXED layout (cap > 0, T <= cap <= 256):
+ * peer p's rows at [p*cap, p*cap + counts[p]), the rest with ids -1 (no counts
+ * exchange, no host sync).  COMPACT layout (cap == 0): peer blocks back to back
+ * at offsets from beam_ep_count's per-tile counts [world][beam_ep_tiles(T)].
+ * send_pos [world, T] = row of (peer, token) or -1. */
+int beam_ep_tiles(int T);
+int beam_ep_count(const int64_t* masked_ids, int T, int K, int N, int world, int32_t* tile_counts,
+                  beam_stream_t stream);
+int beam_ep_pack(const void* h, int h_dtype, int T, int d, const int64_t* masked_ids, const float* weights,
+                 int N, int K, int world, int cap, const int32_t* tile_counts, int has_norm, void* x_send,
+                 int32_t* meta, int32_t* send_pos, int32_t* counts, beam_stream_t stream);
+/* Owner side: the local experts (local->num_experts = N/world, norm_w = the
+ * block's RMS weight or has_norm 0) on n received rows -> y f32 [n, d_h]
+ * (ghat-weighted, ascending local expert id; no residual).  mode: 0 auto,
+ * 1 weight streaming (decode), 2 tcgen05 grouped GEMM. */
+size_t beam_ep_workspace_bytes(const beam_layer_t* local, int n, int K, int mode);
+int beam_ep_execute(const beam_layer_t* local, const void* x, int x_dtype, int n, int K, const int32_t* meta,
+                    int mode, float* y, void* workspace, size_t workspace_bytes, beam_stream_t stream);
+/* Token side: out[t] = h[t] + sum over ranks p ascending of y_back[send_pos[p, t]]. */
+int beam_ep_combine(const float* y_back, const int32_t* send_pos, int world, int T, int d, const void* h,
+                    int h_dtype, void* out, beam_stream_t stream);
+
 /* Fused decode gate phase timestamps (%globaltimer ns) into a device buffer of 16
  * u64 (caller initialises [0],[2] to ~0 and the rest to 0); NULL disables:
  * {first CTA start, last CTA start, first / last projection done,

@@ -50,6 +50,12 @@ EXPORTS = (
     "beam_last_cuda_error",
     "beam_build_info",
     "beam_host_mapped",
+    "beam_ep_tiles",
+    "beam_ep_count",
+    "beam_ep_pack",
+    "beam_ep_workspace_bytes",
+    "beam_ep_execute",
+    "beam_ep_combine",
 )
 
 
@@ -146,6 +152,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_last_cuda_error": (ctypes.c_char_p, []),
         "beam_build_info": (ctypes.c_char_p, []),
         "beam_host_mapped": (I, [P]),
+        "beam_ep_tiles": (I, [I]),
+        "beam_ep_count": (I, [P, I, I, I, I, P, P]),
+        "beam_ep_pack": (I, [P, I, I, I, P, P, I, I, I, I, P, I, P, P, P, P, P]),
+        "beam_ep_workspace_bytes": (S, [LP, I, I, I]),
+        "beam_ep_execute": (I, [LP, P, I, I, I, P, I, P, P, S, P]),
+        "beam_ep_combine": (I, [P, P, I, I, I, P, I, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

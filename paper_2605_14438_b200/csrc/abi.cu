@@ -95,7 +95,9 @@ struct LayerWs {
 
 // One layout serves every entry (sized for the largest user, beam_layer_forward).
 // x_bytes: element size of the activation rows (4 covers both dtypes).
-static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, LayerWs* o, int cols = 0) {
+// force_tc: -1 = the use_tc rule, 0 = weight streaming, 1 = tensor cores (when supported)
+static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, LayerWs* o, int cols = 0,
+                    int force_tc = -1) {
   const Dims g = dims_of(L);
   if (cols < 2 * g.N) cols = 2 * g.N;  // projection columns (router [+ null] [+ mask])
   const int Krow = Kids > g.Keff ? Kids : g.Keff;
@@ -106,7 +108,7 @@ static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, La
   w.counters = c.take<int>(64);
   w.pscratch = c.take<int>(permute_scratch_bytes(T, Krow, g.E) / sizeof(int));
   w.rscratch = T > 64 ? c.take<char>(router_tc_scratch_bytes(cols, g.d_pad)) : nullptr;
-  w.tc = use_tc(L, g, T, Krow);
+  w.tc = force_tc < 0 ? use_tc(L, g, T, Krow) : (force_tc == 1 && tc_supported(L, g));
   w.cap = (int)cap;
   w.xperm = w.tc ? c.take<__nv_bfloat16>(cap * g.d_pad) : nullptr;
   w.act16 = w.tc ? c.take<__nv_bfloat16>(cap * g.f_pad) : nullptr;
@@ -140,6 +142,21 @@ static cudaError_t strided_input(const Dims& g, const void* h, int h_dtype, int 
   }
   *X = w.xpad;
   return launch_pad_rows(h, h_dtype, T, g.d, g.d_pad, w.xpad, h_dtype, s);
+}
+
+// Expert stage on plan `p` for rows X (no norm): the tcgen05 grouped GEMM when
+// the workspace was carved for it (w.tc), else weight streaming.  Returns the
+// dtype of the per-pair rows in w.opair (the combine's input).
+static cudaError_t run_experts(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
+                               const PlanDev& p, LayerWs& w, int* opair_dtype, cudaStream_t s) {
+  cudaError_t e;
+  if (w.tc) {
+    *opair_dtype = BEAM_BF16;
+    if ((e = launch_pack_x(X, x_dtype, nullptr, nullptr, g, p, w.cap, w.xperm, s)) != cudaSuccess) return e;
+    return launch_experts_tc(L, g, w.xperm, p, w.cap, w.act16, w.opair, s);
+  }
+  *opair_dtype = BEAM_F32;
+  return launch_experts_simt(L, g, X, x_dtype, T, p, w.act, w.opair, s);
 }
 
 static int validate(const beam_layer_t* L) {
@@ -418,9 +435,102 @@ int beam_moe_execute(const beam_layer_t* layer, const void* x, int x_dtype, int 
   const void* X = nullptr;
   BEAM_TRY(strided_input(g, x, x_dtype, T, w, &X, s));
   BEAM_TRY(launch_permute<int32_t>(ids, wts, T, K, g.E, 1, w.plan, w.pscratch, s));
-  BEAM_TRY(launch_experts_simt(L, g, X, x_dtype, T, w.plan, w.act, w.opair, s));
-  BEAM_TRY(launch_combine(w.plan, w.opair, BEAM_F32, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
+  int od = BEAM_F32;
+  BEAM_TRY(run_experts(L, g, X, x_dtype, T, w.plan, w, &od, s));
+  BEAM_TRY(launch_combine(w.plan, w.opair, od, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
   return BEAM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// expert parallelism (ep.cu; paper_2605_14438_b200/ep.py)
+// ---------------------------------------------------------------------------
+int beam_ep_tiles(int T) { return T > 0 ? ep_tiles(T) : 0; }
+
+int beam_ep_count(const int64_t* masked_ids, int T, int K, int N, int world, int32_t* tile_counts,
+                  beam_stream_t stream) {
+  if (T < 0 || K < 1 || N < 1 || world < 1 || world > 32 || N % world) return BEAM_ERR_ARG;
+  if (T == 0) return BEAM_OK;
+  if (!masked_ids || !tile_counts) return BEAM_ERR_ARG;
+  return status(launch_ep_count(masked_ids, T, K, N, world, N / world, tile_counts,
+                                reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int beam_ep_pack(const void* h, int h_dtype, int T, int d, const int64_t* masked_ids, const float* weights, int N,
+                 int K, int world, int cap, const int32_t* tile_counts, int has_norm, void* x_send, int32_t* meta,
+                 int32_t* send_pos, int32_t* counts, beam_stream_t stream) {
+  if (T < 0 || d < 1 || K < 1 || N < 1 || world < 1 || world > 32 || N % world || cap < 0) return BEAM_ERR_ARG;
+  if (h_dtype != BEAM_F32 && h_dtype != BEAM_BF16) return BEAM_ERR_ARG;
+  if (cap > 0 && T > cap) return BEAM_ERR_ARG;
+  if (cap > 0 && T > 256) return BEAM_ERR_UNSUPPORTED;  // fixed capacity: decode-sized batches
+  if (cap == 0 && T > 0 && !tile_counts) return BEAM_ERR_ARG;
+  if (T == 0 && cap == 0) return BEAM_OK;  // (fixed layout with T == 0 still fills its empty blocks)
+  if ((T > 0 && (!h || !masked_ids || !weights || !send_pos)) || !x_send || !meta || (cap > 0 && !counts))
+    return BEAM_ERR_ARG;
+  return status(launch_ep_pack(h, h_dtype, T, d, masked_ids, weights, N, K, world, N / world, cap, tile_counts,
+                               has_norm, x_send, meta, send_pos, counts, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+static size_t ep_carve(const beam_layer_t& L, int n, int K, int mode, void* ws, LayerWs* o, float** xw) {
+  const Dims g = dims_of(L);
+  size_t off = carve(L, n, K, 1, ws, o, 0, mode == 1 ? 0 : mode == 2 ? 1 : -1);
+  off = (off + 255) & ~size_t(255);
+  if (xw) *xw = ws ? reinterpret_cast<float*>(static_cast<char*>(ws) + off) : nullptr;
+  return off + (L.has_norm ? (size_t)n * g.d_pad * sizeof(float) : 0) + 256;
+}
+
+size_t beam_ep_workspace_bytes(const beam_layer_t* local, int n, int K, int mode) {
+  if (validate(local) != BEAM_OK || n < 0 || K < 1 || mode < 0 || mode > 2) return 0;
+  LayerWs w;
+  return ep_carve(*local, n, K, mode, nullptr, &w, nullptr);
+}
+
+int beam_ep_execute(const beam_layer_t* local, const void* x, int x_dtype, int n, int K, const int32_t* meta,
+                    int mode, float* y, void* workspace, size_t workspace_bytes, beam_stream_t stream) {
+  int rc = validate(local);
+  if (rc) return rc;
+  if (n < 0 || K < 1 || K > 32 || mode < 0 || mode > 2) return K > 32 ? BEAM_ERR_UNSUPPORTED : BEAM_ERR_ARG;
+  if (x_dtype != BEAM_F32 && x_dtype != BEAM_BF16) return BEAM_ERR_ARG;
+  if (local->num_shared != 0) return BEAM_ERR_ARG;
+  if (n == 0) return BEAM_OK;
+  if (!x || !meta || !y) return BEAM_ERR_ARG;
+  const beam_layer_t& L = *local;
+  const Dims g = dims_of(L);
+  LayerWs w;
+  float* xw = nullptr;
+  if (!workspace || ep_carve(L, n, K, mode, workspace, &w, &xw) > workspace_bytes) return BEAM_ERR_WORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool prescale = L.has_norm && !w.tc;
+  BEAM_TRY(launch_ep_unpack(meta, n, K, x, x_dtype, g.d, g.d_pad, L.norm_w, w.ids32, w.gw, w.inv,
+                            prescale ? xw : nullptr, s));
+  BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, n, K, g.E, 1, w.plan, w.pscratch, s));
+  const float* inv = L.has_norm ? w.inv : nullptr;
+  if (w.tc) {
+    const void* X = nullptr;
+    BEAM_TRY(strided_input(g, x, x_dtype, n, w, &X, s));
+    BEAM_TRY(launch_pack_x(X, x_dtype, inv, L.has_norm ? L.norm_w : nullptr, g, w.plan, w.cap, w.xperm, s));
+    BEAM_TRY(launch_experts_tc(L, g, w.xperm, w.plan, w.cap, w.act16, w.opair, s));
+  } else if (prescale) {
+    BEAM_TRY(launch_gateup_simt(L, g, xw, BEAM_F32, n, inv, nullptr, w.plan, w.act, s, (long long)n * K));
+    BEAM_TRY(launch_down_simt(L, g, n, w.plan, w.act, w.opair, s));
+  } else {
+    const void* X = nullptr;
+    BEAM_TRY(strided_input(g, x, x_dtype, n, w, &X, s));
+    BEAM_TRY(launch_gateup_simt(L, g, X, x_dtype, n, nullptr, nullptr, w.plan, w.act, s));
+    BEAM_TRY(launch_down_simt(L, g, n, w.plan, w.act, w.opair, s));
+  }
+  BEAM_TRY(launch_combine(w.plan, w.opair, w.tc ? BEAM_BF16 : BEAM_F32, n, K, g.d, g.d_pad, nullptr, BEAM_F32, y,
+                          BEAM_F32, s));
+  return BEAM_OK;
+}
+
+int beam_ep_combine(const float* y_back, const int32_t* send_pos, int world, int T, int d, const void* h,
+                    int h_dtype, void* out, beam_stream_t stream) {
+  if (world < 1 || world > 32 || T < 0 || d < 1) return BEAM_ERR_ARG;
+  if (h_dtype != BEAM_F32 && h_dtype != BEAM_BF16) return BEAM_ERR_ARG;
+  if (T == 0) return BEAM_OK;
+  if (!send_pos || !h || !out) return BEAM_ERR_ARG;
+  return status(launch_ep_combine(y_back, send_pos, world, T, d, h, h_dtype, out,
+                                  reinterpret_cast<cudaStream_t>(stream)));
 }
 
 int beam_mask_route(const int64_t* topk_ids, const void* a, int a_dtype, int T, int K, int N,
@@ -496,8 +606,9 @@ int beam_grouped_execute(const beam_layer_t* layer, const void* x, int x_dtype, 
   BEAM_TRY(strided_input(g, x, x_dtype, T, w, &X, s));
   BEAM_TRY(launch_plan_prepare(counts, offsets, tokens, slots, meta, weights_hat, T, K, g.N, p,
                                flags, s));
-  BEAM_TRY(launch_experts_simt(L, g, X, x_dtype, T, p, w.act, w.opair, s));
-  BEAM_TRY(launch_combine(p, w.opair, BEAM_F32, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
+  int od = BEAM_F32;
+  BEAM_TRY(run_experts(L, g, X, x_dtype, T, p, w, &od, s));
+  BEAM_TRY(launch_combine(p, w.opair, od, T, K, g.d, g.d_pad, nullptr, BEAM_F32, y, BEAM_F32, s));
   return BEAM_OK;
 }
 

@@ -159,6 +159,18 @@ cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* ga
 cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* xperm, const PlanDev& p,
                               int cap, void* act16, void* opair, cudaStream_t s);
 
+// ep.cu (expert-parallel dispatch / combine halves around the collectives)
+int ep_tiles(int T);
+cudaError_t launch_ep_count(const int64_t* ids, int T, int K, int N, int world, int n_local, int32_t* tile_counts,
+                            cudaStream_t s);
+cudaError_t launch_ep_pack(const void* h, int h_dtype, int T, int d, const int64_t* ids, const float* weights, int N,
+                           int K, int world, int n_local, int cap, const int32_t* tile_counts, int has_norm,
+                           void* x_send, int32_t* meta, int32_t* send_pos, int32_t* counts, cudaStream_t s);
+cudaError_t launch_ep_unpack(const int32_t* meta, int n, int K, const void* x, int x_dtype, int d, int d_pad,
+                             const float* nw, int32_t* ids32, float* gw, float* inv, float* xw, cudaStream_t s);
+cudaError_t launch_ep_combine(const float* y_back, const int32_t* send_pos, int world, int T, int d, const void* h,
+                              int h_dtype, void* out, cudaStream_t s);
+
 // combine.cu
 cudaError_t launch_combine(const PlanDev& p, const void* opair, int opair_dtype, int T, int Keff, int d, int d_pad,
                            const void* h, int h_dtype, void* out, int out_dtype,

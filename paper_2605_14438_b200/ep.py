@@ -3,35 +3,44 @@
 Not in the reference (expert parallelism is listed as an open limitation,
 PAPER.md:712) — this is the north star's multi-GPU row.
 
-Rank r of P owns the contiguous expert range [r*N/P, (r+1)*N/P).  Every rank
-holds the (small) router and mask router, so gating is replicated; per layer call:
+Rank r of P owns the contiguous expert range [r*N/P, (r+1)*N/P); only those
+experts are ever allocated on it.  The router and mask router (0.5-1 MB each)
+are replicated, so gating is local.  Per layer call (all data-plane work in
+sm_100a kernels, csrc/ep.cu, behind the C ABI):
 
-  1. gate the rank's own T tokens (fused sm_100a gating kernel): surviving
-     (token, slot) pairs with their routing weights ghat;
-  2. dispatch: each token is sent ONCE to every rank that owns at least one of its
-     surviving experts (dedup), with a metadata row [K local ids | K weights];
-     masked slots cost no bytes — BEAM's sparsity shrinks the all-to-all;
-  3. the owner runs its local experts on the received rows (beam_moe_execute:
-     masked permute + weight-streaming / tcgen05 experts + combine);
-  4. combine: partial sums travel back; the token's rank adds them in ascending
-     rank order (= ascending expert ranges), then the residual.
+  1. gate the rank's own T tokens (``beam_gate``): masked ids + weights;
+  2. pack (``beam_ep_pack``, ONE launch): one send row per (token, destination
+     rank) with at least one surviving slot there — deduplicated; masked slots
+     send nothing — holding the raw token row and a metadata row
+     [K local ids | K weights | inv_rms];
+  3. all-to-all of rows and metadata (NCCL over NVLink / NVSwitch);
+  4. the owner runs its local experts on what it received (``beam_ep_execute``:
+     unpack -> masked permute -> weight-streaming or tcgen05 experts -> ordered
+     combine), applying the RMS norm itself, exactly as the single-GPU layer;
+  5. all-to-all of the fp32 partial sums back;
+  6. ``beam_ep_combine``: out = h + partial sums in ascending rank order
+     (= ascending expert ranges, dispatch/__init__.py:145-156).
 
-Collectives: one all-to-all of P ints (counts; the only host sync) and three
-all_to_all_single calls (rows, metadata, partial sums); decode-sized batches
-(T <= 256) use a fixed-capacity variant with no counts exchange and no host
-sync (``ep_exchange_forward_fixed``) — NCCL over NVLink /
-NVSwitch on B200s, gloo in the CPU tests.  Output equals the single-GPU layer up
-to fp32 re-association of the per-token sum across ranks.
+Two protocols, chosen identically on every rank:
+  * FIXED capacity (decode, T <= 256 per rank): every peer gets a block of
+    `cap` rows (unused rows carry id -1 and cost no expert work); no counts
+    exchange and no host sync, so the whole step — collectives included —
+    replays as one CUDA graph.  `cap` is the layer's ``capacity`` (a static
+    serving contract, same on every rank) or, without one, the max T over the
+    ranks (one all-reduce).
+  * COMPACT (prefill): per-destination counts (``beam_ep_count``) are exchanged
+    first (the one host sync), then variable-split all-to-alls — BEAM's masked
+    slots shrink the exchange.
 
-The exchange logic is device-agnostic and takes the gating and local-expert
-compute as callables, so tests/test_ep_gloo.py runs it with world_size 2 on CPU
-with the oracle as the local compute.
+Output equals the single-GPU layer up to fp32 re-association of the per-token
+sum across rank boundaries.  ``virtual_forward`` runs P shards in ONE process
+with a loopback exchange (SURVEY §4 "virtual EP"); the host-side protocol is
+covered with gloo on CPU by tests/test_ep_gloo.py (oracle kernels injected).
 """
 
 from __future__ import annotations
 
 import ctypes
-import math
 import os
 import time
 from dataclasses import dataclass
@@ -41,178 +50,328 @@ import torch
 import torch.distributed as dist
 
 from . import _lib, _runtime
-
-
-@dataclass
-class Gated:
-    xn: torch.Tensor     # [T, d] normalised activations (what the experts consume)
-    ids: torch.Tensor    # [T, K] int64 surviving expert ids, -1 = masked
-    ghat: torch.Tensor   # [T, K] f32 routing weight of each slot (0 where masked)
-
+from .tensor import ContractError, ShapeError
 
 FIXED_CAPACITY_MAX_T = 256  # decode-sized batches use the sync-free fixed-capacity exchange
 
 
-def ep_exchange_forward_fixed(h: torch.Tensor, gated: Gated, num_experts: int, local_fn, group=None) -> torch.Tensor:
-    """Steps 2-4 with a fixed-capacity protocol (no counts exchange, no host
-    sync): every rank sends each peer one row per token — the rows a peer owns
-    no surviving expert of carry only -1 ids, so the peer's masked permute skips
-    them (no expert bytes or FLOPs; the exchange costs T rows per peer, a few MB
-    at decode sizes).  Partial sums come back the same way and are added in
-    ascending rank order."""
-    world = dist.get_world_size(group)
-    if num_experts % world:
-        raise ValueError("num_experts must divide evenly across ranks")
-    n_local = num_experts // world
-    t, k = gated.ids.shape
-    d = gated.xn.shape[1]
-    dev = h.device
-    ids = gated.ids
-    ranks = torch.arange(world, device=dev).view(world, 1, 1)
-    owner = torch.where(ids >= 0, ids // n_local, torch.full_like(ids, -1))[None]            # [1, T, K]
-    mine = owner == ranks                                                                     # [P, T, K]
-    loc_ids = torch.where(mine, ids[None] - ranks * n_local, torch.full_like(ids[None], -1))
-    loc_w = torch.where(mine, gated.ghat[None].to(torch.float32), torch.zeros((), device=dev))
-    meta = torch.cat([loc_ids.to(torch.int32), loc_w.view(torch.int32)], dim=2).reshape(world * t, 2 * k).contiguous()
-    x_send = gated.xn[None].expand(world, t, d).reshape(world * t, d).contiguous()
-    x_recv = torch.empty_like(x_send)
-    meta_recv = torch.empty_like(meta)
-    dist.all_to_all_single(x_recv, x_send, group=group)
-    dist.all_to_all_single(meta_recv, meta, group=group)
-    y_recv = local_fn(x_recv, meta_recv[:, :k].contiguous(), meta_recv[:, k:].contiguous().view(torch.float32))
-    y_recv = y_recv.to(torch.float32).contiguous()
-    y_back = torch.empty_like(y_recv)
-    dist.all_to_all_single(y_back, y_recv, group=group)
-    y_back = y_back.view(world, t, d)
-    y = y_back[0].clone()
-    for r in range(1, world):  # ascending rank == ascending expert range
-        y += y_back[r]
-    return (h.to(torch.float32) + y).to(h.dtype)
+@dataclass
+class Sent:
+    """One rank's packed send buffers."""
+
+    x: torch.Tensor          # [rows, d] raw token rows (h dtype)
+    meta: torch.Tensor       # [rows, 2K+1] int32
+    send_pos: torch.Tensor   # [P, T] int32: row of (peer, token) or -1
+    cap: int                 # fixed layout: rows per peer; 0 = compact
+    splits: list | None      # compact: rows per peer (host ints)
 
 
-def ep_exchange_forward(h: torch.Tensor, gated: Gated, num_experts: int, local_fn, group=None) -> torch.Tensor:
-    """Steps 2-4 above.  ``local_fn(x [n, d], ids [n, K] int32 local ids (-1 skip),
-    w [n, K] f32) -> y [n, d] f32`` runs this rank's experts.  Returns h + y in
-    h's dtype."""
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    if num_experts % world:
-        raise ValueError("num_experts must divide evenly across ranks")
-    n_local = num_experts // world
-    t, k = gated.ids.shape
-    dev = h.device
-    ids = gated.ids
-    dest = torch.where(ids >= 0, ids // n_local, torch.full_like(ids, -1))            # [T, K]
-    send_mask = torch.stack([(dest == r).any(dim=1) for r in range(world)])             # [P, T]
-    pairs = send_mask.nonzero()                                                          # (r, t) rank-major
-    r_idx, t_idx = pairs[:, 0], pairs[:, 1]
-    counts_send = send_mask.sum(dim=1).to(torch.int64)
-    # metadata: local ids of the slots that belong to the destination, and their weights
-    mine = dest[t_idx] == r_idx[:, None]                                                 # [n, K]
-    loc_ids = torch.where(mine, ids[t_idx] - r_idx[:, None] * n_local, torch.full_like(ids[t_idx], -1))
-    loc_w = torch.where(mine, gated.ghat[t_idx], torch.zeros_like(gated.ghat[t_idx]))
-    meta = torch.cat([loc_ids.to(torch.int32), loc_w.to(torch.float32).view(torch.int32)], dim=1).contiguous()
-    x_send = gated.xn[t_idx].contiguous()
-
-    counts_recv = torch.empty_like(counts_send)
-    dist.all_to_all_single(counts_recv, counts_send, group=group)
-    send_splits = counts_send.tolist()
-    recv_splits = counts_recv.tolist()
-    n_recv = int(sum(recv_splits))
-    x_recv = torch.empty((n_recv, x_send.shape[1]), dtype=x_send.dtype, device=dev)
-    meta_recv = torch.empty((n_recv, 2 * k), dtype=torch.int32, device=dev)
-    dist.all_to_all_single(x_recv, x_send, recv_splits, send_splits, group=group)
-    dist.all_to_all_single(meta_recv, meta, recv_splits, send_splits, group=group)
-
-    ids_recv = meta_recv[:, :k].contiguous()
-    w_recv = meta_recv[:, k:].contiguous().view(torch.float32)
-    y_recv = local_fn(x_recv, ids_recv, w_recv) if n_recv else torch.zeros((0, x_send.shape[1]), device=dev)
-    y_recv = y_recv.to(torch.float32).contiguous()
-
-    y_back = torch.empty((int(sum(send_splits)), y_recv.shape[1]), dtype=torch.float32, device=dev)
-    dist.all_to_all_single(y_back, y_recv, send_splits, recv_splits, group=group)
-
-    # ascending rank == ascending expert range; each rank's rows have unique tokens
-    y = torch.zeros((t, h.shape[1]), dtype=torch.float32, device=dev)
-    start = 0
-    for r in range(world):
-        n = send_splits[r]
-        if n:
-            y[t_idx[start : start + n]] += y_back[start : start + n]
-        start += n
-    return (h.to(torch.float32) + y).to(h.dtype)
+# ---------------------------------------------------------------------------
+# device kernels through the C ABI (backend-independent host logic is below)
+# ---------------------------------------------------------------------------
 
 
-class EPBeamLayer:
-    """One BEAM MoE layer sharded over the ranks of ``group`` (CUDA + NCCL).
+class DeviceKernels:
+    """The product data plane: pack / local execute / combine on the GPU."""
 
-    ``block`` is a full-size ``MoEBlock`` description used only for its routers /
-    norm (replicated); only this rank's experts are kept on the device."""
+    def __init__(self, layer: "EPBeamLayer"):
+        self.L = layer
 
-    def __init__(self, block, group=None):
-        from .moe import MoEBlock, MoEBlockConfig
-
-        self.group = group
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        cfg = block.cfg
-        if cfg.num_experts % self.world:
-            raise ValueError("num_experts must divide evenly across ranks")
-        if cfg.num_shared:
-            raise ValueError("shared experts are not sharded by the EP path")
-        self.cfg = cfg
-        self.n_local = cfg.num_experts // self.world
-        self.block = block
-        lo = self.rank * self.n_local
-        lcfg = MoEBlockConfig(cfg.d_h, cfg.d_ff, self.n_local, 1, 0, False, cfg.activation)
-        self.local = MoEBlock(lcfg, dtype=block.dtype, device=block.device, _empty=True)
-        self.local.w_gu.copy_(block.w_gu[lo : lo + self.n_local])
-        self.local.w_down.copy_(block.w_down[lo : lo + self.n_local])
-
-    def gate(self, h: torch.Tensor) -> Gated:
+    def gate(self, h):
+        """beam_gate with the replicated routers: (masked ids [T, K] int64,
+        router weights [T, N] f32)."""
         from .beam import _threshold
-        from .moe import _gate_call  # noqa: F401  (same C entry, full router)
 
-        blk = self.block
+        L = self.L
+        blk = L.router
         desc = blk.layer_desc(_threshold(blk.mask_router.tau))
         t = h.shape[0]
-        n, k = self.cfg.num_experts, self.cfg.top_k
+        n, k = L.cfg.num_experts, L.cfg.top_k
         masked = torch.empty(t, k, dtype=torch.int64, device=h.device)
         weights = torch.empty(t, n, dtype=torch.float32, device=h.device)
+        if t == 0:
+            return masked, weights
         o = _lib.Outputs()
         o.masked_ids = masked.data_ptr()
         o.weights = weights.data_ptr()
         lib = _lib.load()
         ws = _runtime.workspace(lib.beam_workspace_bytes(ctypes.byref(desc), t, 0, 1), h.device)
-        _lib.check(lib.beam_gate(ctypes.byref(desc), h.data_ptr(),
-                                 _lib.BEAM_BF16 if h.dtype == torch.bfloat16 else _lib.BEAM_F32, t,
-                                 ctypes.byref(o), ws.data_ptr(), ws.numel(), _runtime.stream_handle(h.device)),
-                   "beam_gate")
-        ghat = torch.where(masked >= 0, torch.gather(weights, 1, masked.clamp(min=0)), torch.zeros((), device=h.device))
-        xn = blk.normalize(h).to(blk.dtype) if blk.norm_w is not None else h.to(blk.dtype)
-        return Gated(xn=xn, ids=masked, ghat=ghat)
+        _lib.check(lib.beam_gate(ctypes.byref(desc), h.data_ptr(), _dt(h), t, ctypes.byref(o), ws.data_ptr(),
+                                 ws.numel(), _runtime.stream_handle(h.device)), "beam_gate")
+        return masked, weights
 
-    def local_fn(self, x, ids, w):
-        from .dispatch import execute_routed
+    def counts(self, masked):
+        """Rows per destination rank (int64 [P], device) for the compact layout,
+        and the per-tile counts the pack kernel reads."""
+        L = self.L
+        t = masked.shape[0]
+        lib = _lib.load()
+        tiles = torch.zeros(L.world, max(lib.beam_ep_tiles(t), 1), dtype=torch.int32, device=masked.device)
+        if t:
+            _lib.check(lib.beam_ep_count(masked.data_ptr(), t, L.cfg.top_k, L.cfg.num_experts, L.world,
+                                         tiles.data_ptr(), _runtime.stream_handle(masked.device)), "beam_ep_count")
+        return tiles.sum(dim=1, dtype=torch.int64), tiles
 
-        return execute_routed(self.local, x.contiguous(), ids.contiguous(), w.contiguous())
+    def pack(self, h, masked, weights, cap, tiles=None, rows=None):
+        L = self.L
+        t, d = h.shape
+        k = L.cfg.top_k
+        dev = h.device
+        n_rows = L.world * cap if cap > 0 else rows
+        x = torch.empty(n_rows, d, dtype=h.dtype, device=dev)
+        meta = torch.empty(n_rows, 2 * k + 1, dtype=torch.int32, device=dev)
+        send_pos = torch.empty(L.world, t, dtype=torch.int32, device=dev)
+        counts = torch.empty(L.world, dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().beam_ep_pack(
+            h.data_ptr() if t else None, _dt(h), t, d, masked.data_ptr() if t else None,
+            weights.data_ptr() if t else None, L.cfg.num_experts, k, L.world, cap,
+            tiles.data_ptr() if tiles is not None else None, 1 if L.cfg.has_norm else 0, x.data_ptr(),
+            meta.data_ptr(), send_pos.data_ptr() if t else None, counts.data_ptr(), _runtime.stream_handle(dev)),
+            "beam_ep_pack")
+        return x, meta, send_pos
 
-    def forward(self, h: torch.Tensor) -> torch.Tensor:
-        h = h.contiguous()
-        fwd = ep_exchange_forward_fixed if h.shape[0] <= FIXED_CAPACITY_MAX_T else ep_exchange_forward
-        return fwd(h, self.gate(h), self.cfg.num_experts, self.local_fn, self.group)
+    def local(self, x, meta, mode):
+        """Owner side: y f32 [n, d] = this rank's experts on the received rows."""
+        L = self.L
+        n = x.shape[0]
+        y = torch.empty(n, L.cfg.d_h, dtype=torch.float32, device=x.device)
+        if n == 0:
+            return y
+        desc = L.local.layer_desc(0.0)
+        lib = _lib.load()
+        ws = _runtime.workspace(lib.beam_ep_workspace_bytes(ctypes.byref(desc), n, L.cfg.top_k, mode), x.device)
+        _lib.check(lib.beam_ep_execute(ctypes.byref(desc), x.data_ptr(), _dt(x), n, L.cfg.top_k, meta.data_ptr(),
+                                       mode, y.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       _runtime.stream_handle(x.device)), "beam_ep_execute")
+        return y
+
+    def combine(self, h, y_back, send_pos):
+        out = torch.empty_like(h)
+        t = h.shape[0]
+        if t:
+            _lib.check(_lib.load().beam_ep_combine(y_back.data_ptr() if y_back.numel() else None,
+                                                   send_pos.data_ptr(), self.L.world, t, h.shape[1],
+                                                   h.data_ptr(), _dt(h), out.data_ptr(),
+                                                   _runtime.stream_handle(h.device)), "beam_ep_combine")
+        return out
+
+
+def _dt(x):
+    return _lib.BEAM_BF16 if x.dtype == torch.bfloat16 else _lib.BEAM_F32
 
 
 # ---------------------------------------------------------------------------
-# bench.py --gpus N (torchrun): EP at the Qwen3-30B-A3B shape, T tokens per rank
+# the sharded layer
+# ---------------------------------------------------------------------------
+
+
+class EPBeamLayer:
+    """One BEAM MoE layer sharded over ranks: this rank's experts + replicated routers.
+
+    ``local_experts`` = (w_gate [n_local, d, f], w_up [n_local, d, f], w_down
+    [n_local, f, d]) of THIS rank's expert range only (host or device tensors;
+    packed straight into the rank's device layout — the full block is never
+    built).  ``capacity``: static max tokens per rank per call (decode serving
+    contract, identical on every rank): the fixed-capacity protocol with no host
+    sync; None = agree on the protocol per call (one all-reduce)."""
+
+    def __init__(self, cfg, router_w, mask_w, local_experts, *, norm_w=None, tau: float = 0.5, group=None,
+                 rank: int | None = None, world: int | None = None, capacity: int | None = None,
+                 dtype=torch.bfloat16, device=None, kernels=None):
+        from .beam import MaskRouter
+        from .moe import MoEBlock, MoEBlockConfig
+
+        self.group = group
+        self.world = world if world is not None else dist.get_world_size(group)
+        self.rank = rank if rank is not None else dist.get_rank(group)
+        if cfg.num_experts % self.world:
+            raise ContractError("num_experts must divide evenly across ranks")
+        if cfg.num_shared:
+            raise ContractError("shared experts are not sharded by the EP path")
+        if capacity is not None and not 1 <= capacity <= FIXED_CAPACITY_MAX_T:
+            raise ContractError(f"capacity must lie in [1, {FIXED_CAPACITY_MAX_T}]")
+        self.cfg = cfg
+        self.capacity = capacity
+        self.n_local = cfg.num_experts // self.world
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        # replicated gating: routers + norm, no expert storage
+        self.router = MoEBlock(cfg, dtype=dtype, device=dev, _router_only=True)
+        self.router.router_w.copy_(torch.as_tensor(router_w, dtype=torch.float32))
+        if self.router.norm_w is not None and norm_w is not None:
+            self.router.norm_w.copy_(torch.as_tensor(norm_w, dtype=torch.float32))
+        self.router.mask_router = MaskRouter(torch.as_tensor(mask_w, dtype=torch.float32).to(dev), tau)
+        # this rank's experts (norm weight applied by the owner, beam_ep_execute)
+        lcfg = MoEBlockConfig(cfg.d_h, cfg.d_ff, self.n_local, 1, 0, cfg.has_norm, cfg.activation)
+        self.local = MoEBlock(lcfg, dtype=dtype, device=dev, _empty=True)
+        if self.local.norm_w is not None:
+            self.local.norm_w.copy_(self.router.norm_w)
+        g, u, dn = local_experts
+        if g.shape[0] != self.n_local:
+            raise ShapeError(f"expected {self.n_local} local experts, got {g.shape[0]}")
+        self.local._set_all_experts((g, u, dn), 0, self.n_local)
+        # the data-plane kernels: the CUDA library; the CPU protocol tests inject a
+        # host restatement (oracle/ep_oracle.py) through this factory
+        self.kernels = (kernels or DeviceKernels)(self)
+        self._staged = dist.is_initialized() and dist.get_backend(group) == "gloo" and dev.type == "cuda"
+
+    @classmethod
+    def from_block(cls, block, group=None, *, rank=None, world=None, capacity=None) -> "EPBeamLayer":
+        """Shard of a full single-GPU block (tests / comparisons): this rank's
+        slice of its experts, its routers and norm."""
+        from .moe import unpack_gate_up
+
+        world = world if world is not None else dist.get_world_size(group)
+        rank = rank if rank is not None else dist.get_rank(group)
+        cfg = block.cfg
+        nl = cfg.num_experts // world
+        lo = rank * nl
+        g, u = unpack_gate_up(block.w_gu[lo:lo + nl], cfg.d_h, cfg.d_ff)
+        dn = block.w_down[lo:lo + nl, :cfg.d_h, :cfg.d_ff].transpose(1, 2)
+        return cls(cfg, block.router_w, block.mask_router.weight, (g, u, dn), norm_w=block.norm_w,
+                   tau=block.mask_router.tau, group=group, rank=rank, world=world, capacity=capacity,
+                   dtype=block.dtype, device=block.device)
+
+    @classmethod
+    def random(cls, cfg, seed: int, *, group=None, rank=None, world=None, capacity=None, dtype=torch.bfloat16,
+               device=None, mask_std: float | None = None) -> "EPBeamLayer":
+        """Random-init shard (N(0, 0.02) experts, bench workloads): expert e is
+        drawn from its own generator (seed, e), so every rank draws only its own
+        experts and any sharding holds the same layer."""
+        world = world if world is not None else dist.get_world_size(group)
+        rank = rank if rank is not None else dist.get_rank(group)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        nl = cfg.num_experts // world
+        d, f = cfg.d_h, cfg.d_ff
+        gr = torch.Generator().manual_seed(seed)
+        router = torch.empty(d, cfg.num_experts).normal_(0.0, 0.02, generator=gr)
+        router[0] = 0.0
+        mask = torch.empty(d, cfg.num_experts).normal_(0.0, mask_std or 1.0 / np.sqrt(d), generator=gr)
+        mask[0] = 0.0
+        gs, us, ds = [], [], []
+        for e in range(rank * nl, (rank + 1) * nl):
+            ge = torch.Generator(device=dev).manual_seed(seed * 1_000_003 + e)
+            gs.append(torch.empty(d, f, device=dev).normal_(0.0, 0.02, generator=ge).to(dtype))
+            us.append(torch.empty(d, f, device=dev).normal_(0.0, 0.02, generator=ge).to(dtype))
+            ds.append(torch.empty(f, d, device=dev).normal_(0.0, 0.02, generator=ge).to(dtype))
+        return cls(cfg, router, mask, (torch.stack(gs), torch.stack(us), torch.stack(ds)), group=group, rank=rank,
+                   world=world, capacity=capacity, dtype=dtype, device=dev)
+
+    # -- collectives (gloo process groups with CUDA tensors stage through host memory)
+    def _a2a(self, out, inp, out_splits=None, in_splits=None):
+        if not self._staged:
+            dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+            return
+        wire = {2: torch.int16, 4: torch.int32, 8: torch.int64}[inp.element_size()]
+        o = torch.empty(out.shape, dtype=out.dtype).view(wire)
+        dist.all_to_all_single(o, inp.cpu().view(wire), out_splits, in_splits, group=self.group)
+        out.copy_(o.view(out.dtype))
+
+    def _protocol(self, t: int):
+        """(cap, fixed): the same on every rank."""
+        if self.capacity is not None:
+            if t > self.capacity:
+                raise ContractError(f"{t} tokens exceed the layer's fixed capacity {self.capacity}")
+            return self.capacity, True
+        tt = torch.tensor([t], dtype=torch.int64, device="cpu" if self._staged or self.device.type != "cuda"
+                          else self.device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX, group=self.group)
+        t_max = int(tt.item())
+        if t_max <= FIXED_CAPACITY_MAX_T:
+            return max(t_max, 1), True
+        return 0, False
+
+    # -- the step
+    def send(self, h, cap: int) -> Sent:
+        """Gate + pack into the fixed-capacity layout (`cap` rows per peer)."""
+        masked, weights = self.kernels.gate(h)
+        x, meta, pos = self.kernels.pack(h, masked, weights, cap)
+        return Sent(x, meta, pos, cap, None)
+
+    def forward(self, h: torch.Tensor) -> torch.Tensor:
+        h = h.contiguous()
+        if h.ndim != 2 or h.shape[1] != self.cfg.d_h:
+            raise ShapeError("h must be [tokens, d_h]")
+        cap, fixed = self._protocol(h.shape[0])
+        k = self.cfg.top_k
+        if fixed:
+            snd = self.send(h, cap)
+            x_recv, meta_recv = torch.empty_like(snd.x), torch.empty_like(snd.meta)
+            self._a2a(x_recv, snd.x)
+            self._a2a(meta_recv, snd.meta)
+            y = self.kernels.local(x_recv, meta_recv, 1)
+            y_back = torch.empty_like(y)
+            self._a2a(y_back, y)
+            return self.kernels.combine(h, y_back, snd.send_pos)
+        masked, weights = self.kernels.gate(h)
+        counts, tiles = self.kernels.counts(masked)
+        counts_recv = torch.empty_like(counts)
+        self._a2a(counts_recv, counts)
+        send_splits = counts.tolist()           # the compact protocol's one host sync
+        recv_splits = counts_recv.tolist()
+        x, meta, pos = self.kernels.pack(h, masked, weights, 0, tiles=tiles, rows=int(sum(send_splits)))
+        n_recv = int(sum(recv_splits))
+        x_recv = torch.empty(n_recv, h.shape[1], dtype=h.dtype, device=h.device)
+        meta_recv = torch.empty(n_recv, 2 * k + 1, dtype=torch.int32, device=h.device)
+        self._a2a(x_recv, x, recv_splits, send_splits)
+        self._a2a(meta_recv, meta, recv_splits, send_splits)
+        y = self.kernels.local(x_recv, meta_recv, 0)
+        y_back = torch.empty(x.shape[0], h.shape[1], dtype=y.dtype, device=h.device)
+        self._a2a(y_back, y, send_splits, recv_splits)
+        return self.kernels.combine(h, y_back, pos)
+
+    __call__ = forward
+
+
+def virtual_forward(layers: list, hs: list, fixed: bool | None = None) -> list:
+    """SURVEY §4 "virtual EP": P shards (``layers[r]``, world = P) in ONE process
+    with a loopback exchange — the pack / execute / combine kernels and the
+    protocols' row bookkeeping exactly as in ``forward``, no process group.
+    Returns every rank's output."""
+    world = len(layers)
+    t_max = max(h.shape[0] for h in hs)
+    if fixed is None:
+        fixed = t_max <= FIXED_CAPACITY_MAX_T
+    if fixed:
+        cap = max(t_max, 1)
+        sent = [ly.send(h.contiguous(), cap) for ly, h in zip(layers, hs)]
+        # rank r receives block r of every peer p's send buffer, in peer order
+        recv = [(torch.cat([s.x[r * cap:(r + 1) * cap] for s in sent]),
+                 torch.cat([s.meta[r * cap:(r + 1) * cap] for s in sent])) for r in range(world)]
+        ys = [layers[r].kernels.local(x, m, 1) for r, (x, m) in enumerate(recv)]
+        backs = [torch.cat([ys[r][p * cap:(p + 1) * cap] for r in range(world)]) for p in range(world)]
+        return [ly.kernels.combine(h.contiguous(), yb, s.send_pos) for ly, h, yb, s in zip(layers, hs, backs, sent)]
+    packs = []
+    for ly, h in zip(layers, hs):
+        h = h.contiguous()
+        masked, weights = ly.kernels.gate(h)
+        counts, tiles = ly.kernels.counts(masked)
+        splits = counts.tolist()
+        x, meta, pos = ly.kernels.pack(h, masked, weights, 0, tiles=tiles, rows=int(sum(splits)))
+        offs = np.concatenate([[0], np.cumsum(splits)]).astype(int)
+        packs.append((h, x, meta, pos, splits, offs))
+    ys, src = [], []
+    for r in range(world):
+        xr = torch.cat([p[1][p[5][r]:p[5][r + 1]] for p in packs])
+        mr = torch.cat([p[2][p[5][r]:p[5][r + 1]] for p in packs])
+        ys.append(layers[r].kernels.local(xr, mr, 0))
+        src.append(np.concatenate([[0], np.cumsum([p[4][r] for p in packs])]).astype(int))
+    outs = []
+    for p_rank, (h, x, meta, pos, splits, offs) in enumerate(packs):
+        yb = torch.cat([ys[r][src[r][p_rank]:src[r][p_rank + 1]] for r in range(world)]) if world else None
+        outs.append(layers[p_rank].kernels.combine(h, yb, pos))
+    return outs
+
+
+# ---------------------------------------------------------------------------
+# bench.py --gpus N (torchrun): EP at the BASELINE shapes, T tokens per rank
 # ---------------------------------------------------------------------------
 
 
 def _capture_step(layer, x, dev):
-    """Decode-sized steps (fixed-capacity exchange: no host sync) replay as one
-    CUDA graph, NCCL collectives included — the eager step is host-launch bound.
-    Returns (graph, graph output) or (None, None) when the step is not captured."""
-    if x.shape[0] > FIXED_CAPACITY_MAX_T or os.environ.get("BEAM_EP_NO_GRAPH") == "1":
+    """Fixed-capacity steps (no host sync) replay as one CUDA graph, NCCL
+    collectives included.  Returns (graph, graph output) or (None, None)."""
+    if layer.capacity is None or os.environ.get("BEAM_EP_NO_GRAPH") == "1":
         return None, None
     try:
         side = torch.cuda.Stream(dev)
@@ -254,9 +413,20 @@ def _timed_total(step, steps, flush):
     return total
 
 
+def _theta_layer(layer, bench, t, s, seed=7):
+    """Calibrate the mask router's row 0 to sparsity s on the rank's tokens
+    (same tokens on every rank's calibration: identical routers everywhere)."""
+    d, k = layer.cfg.d_h, layer.cfg.top_k
+    router = layer.router.router_w.cpu()
+    mask = layer.router.mask_router.weight.cpu()
+    theta = bench.calibrate_theta(bench.make_tokens(t, seed, d), router, mask, k, s)
+    layer.router.mask_router.weight.copy_(bench.mask_with_theta(mask, theta).to(layer.device))
+
+
 def _ep_shape_points(args, bench, dev, flush, world, rank):
     """EP lines for the other BASELINE shapes (configs[3] OLMoE, configs[4]
-    Qwen3-235B): device ms per step, max over ranks, T tokens per rank."""
+    Qwen3-235B): device ms per step, max over ranks, T tokens per rank.  Every
+    rank allocates only its own experts (EPBeamLayer.random)."""
     import paper_2605_14438_b200 as B
 
     rows = []
@@ -265,13 +435,10 @@ def _ep_shape_points(args, bench, dev, flush, world, rank):
         sh = bench.SHAPES[name]
         if sh["n"] % world:
             continue
-        w = bench.shape_layer(B, name, dev)
-        blk = w["_block"]
-        theta = bench.calibrate_theta(bench.make_tokens(t, 7, sh["d"]), w["router"], w["mask"], sh["k"], s)
-        blk.mask_router.weight.copy_(bench.mask_with_theta(w["mask"], theta).to(dev))
-        layer = EPBeamLayer(blk)
-        blk.w_gu = torch.zeros(1, dtype=torch.bfloat16, device=dev)
-        blk.w_down = torch.zeros(1, dtype=torch.bfloat16, device=dev)
+        cfg = B.MoEBlockConfig(d_h=sh["d"], d_ff=sh["f"], num_experts=sh["n"], top_k=sh["k"])
+        layer = EPBeamLayer.random(cfg, 2605, rank=rank, world=world, device=dev,
+                                   capacity=t if t <= FIXED_CAPACITY_MAX_T else None)
+        _theta_layer(layer, bench, t, s)
         x = bench.make_tokens(t, 7 + rank, sh["d"]).to(dev)
         for _ in range(2):
             layer.forward(x)
@@ -285,8 +452,9 @@ def _ep_shape_points(args, bench, dev, flush, world, rank):
         ms = float(t_max.item()) / steps
         rows.append({"shape": name, **sh, "T_per_rank": t, "s_target": s, "ep": world,
                      "experts_per_rank": sh["n"] // world, "ms_per_step": round(ms, 4),
-                     "tokens_per_s": round(world * t / (ms / 1e3), 1), "graph": graph is not None})
-        del layer, blk, w, graph, step
+                     "tokens_per_s": round(world * t / (ms / 1e3), 1), "graph": graph is not None,
+                     "protocol": "fixed" if layer.capacity else "compact"})
+        del layer, graph, step
         torch.cuda.empty_cache()
     return rows
 
@@ -307,15 +475,15 @@ def bench_main(args, bench):
     dist.init_process_group("nccl", device_id=dev)
     q = bench.Q30
     cfg = B.MoEBlockConfig(d_h=q["d"], d_ff=q["f"], num_experts=q["n"], top_k=q["k"])
-    w = bench.make_layer0()
+    w = bench.make_layer0()  # host tensors; only this rank's expert slice goes to the device
     h = bench.make_tokens(args.tokens, 7 + rank)
     theta = bench.calibrate_theta(bench.make_tokens(args.tokens, 7), w["router"], w["mask"], q["k"], args.sparsity)
-    blk = B.MoEBlock.from_weights(cfg, w["router"], (w["wg"], w["wu"], w["wd"]),
-                                  mask_w=bench.mask_with_theta(w["mask"], theta), dtype=torch.bfloat16, device=dev)
-    layer = EPBeamLayer(blk)
-    # only the local shard stays resident (the gate never reads expert weights)
-    blk.w_gu = torch.zeros(1, dtype=torch.bfloat16, device=dev)
-    blk.w_down = torch.zeros(1, dtype=torch.bfloat16, device=dev)
+    nl = q["n"] // world
+    sl = slice(rank * nl, (rank + 1) * nl)
+    layer = EPBeamLayer(cfg, w["router"], bench.mask_with_theta(w["mask"], theta),
+                        (w["wg"][sl], w["wu"][sl], w["wd"][sl]), device=dev,
+                        capacity=args.tokens if args.tokens <= FIXED_CAPACITY_MAX_T else None)
+    del w
     x = h.to(dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     lib = _lib.load()
@@ -323,7 +491,7 @@ def bench_main(args, bench):
         layer.forward(x)
     torch.cuda.synchronize()
     c0 = lib.beam_kernel_launches()
-    layer.forward(x)  # launches of one step through the C ABI (gate + local experts)
+    layer.forward(x)  # launches of one step through the C ABI (gate, pack, local experts, combine)
     torch.cuda.synchronize()
     launches_per_step = int(lib.beam_kernel_launches() - c0)
     graph, y_graph = _capture_step(layer, x, dev)
@@ -362,13 +530,15 @@ def bench_main(args, bench):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
-            "config": {"workload": f"Qwen3-30B-A3B MoE layer, expert parallel EP{world}, T={args.tokens} tokens/rank, "
-                                   f"s={args.sparsity}", **q, "parallelism": f"ep{world}",
-                       "experts_per_rank": q["n"] // world, "l2": "flushed before every step",
-                       "timing": "CUDA events per step, max over ranks" + (
-                           ", CUDA-graph replay of the step (NCCL collectives captured)" if graph is not None
-                           else ", eager step"),
-                       "exchange": "NCCL all_to_all_single (counts, rows, metadata, partial sums)"},
+            "config": bench.workload_config(args.tokens, args.sparsity),
+            "measurement": {"parallelism": f"expert parallel EP{world}, T={args.tokens} tokens per rank",
+                            "experts_per_rank": q["n"] // world, "l2": "flushed before every step",
+                            "protocol": "fixed capacity" if layer.capacity else "compact (counts exchange)",
+                            "timing": "CUDA events per step, max over ranks" + (
+                                ", CUDA-graph replay of the step (NCCL collectives captured)" if graph is not None
+                                else ", eager step"),
+                            "exchange": "device pack/combine kernels (beam_ep_pack / beam_ep_combine) around NCCL "
+                                        "all_to_all_single (rows, metadata, partial sums)"},
             "e2e": {"value": world * args.tokens / e2e_s, "unit": "tokens/s",
                     "h2d_bytes_per_step": world * int(h.numel()) * h.element_size(),
                     "d2h_bytes_per_step": world * int(h.numel()) * h.element_size(),

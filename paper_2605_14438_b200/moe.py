@@ -184,7 +184,8 @@ class MoEBlock:
 
     def __init__(self, cfg: MoEBlockConfig, rng: np.random.Generator | None = None,
                  extra_router_cols: int = 0, init_std: float = 0.02, *,
-                 dtype: torch.dtype = torch.bfloat16, device=None, _empty: bool = False):
+                 dtype: torch.dtype = torch.bfloat16, device=None, _empty: bool = False,
+                 _router_only: bool = False):
         if extra_router_cols < 0:
             raise ContractError("extra_router_cols must be >= 0")
         if dtype not in (torch.bfloat16, torch.float32):
@@ -193,8 +194,16 @@ class MoEBlock:
         self.dtype = dtype
         self.device = torch.device(device) if device is not None else _default_device()
         n_all = cfg.num_experts + cfg.num_shared
-        self.w_gu = torch.zeros(n_all, 2 * cfg.f_pad, cfg.d_pad, dtype=dtype, device=self.device)
-        self.w_down = torch.zeros(n_all, cfg.d_pad, cfg.f_pad, dtype=dtype, device=self.device)
+        if _router_only:
+            # gating only (expert-parallel ranks): the gate kernels never read the
+            # expert weights, so none are allocated (placeholders keep the
+            # descriptor's pointers valid)
+            self.w_gu = torch.zeros(1, dtype=dtype, device=self.device)
+            self.w_down = torch.zeros(1, dtype=dtype, device=self.device)
+            _empty = True
+        else:
+            self.w_gu = torch.zeros(n_all, 2 * cfg.f_pad, cfg.d_pad, dtype=dtype, device=self.device)
+            self.w_down = torch.zeros(n_all, cfg.d_pad, cfg.f_pad, dtype=dtype, device=self.device)
         # moe.py:164-178: num_experts + extra_router_cols columns (the extra ones are the
         # null experts of ada_moe routing, baselines.py:212-225)
         self.extra_router_cols = extra_router_cols
