@@ -90,7 +90,10 @@ typedef struct {
  *           packed row 32*b + i (i<16) = gate feature 16*b+i, 32*b+16+i = up feature 16*b+i
  *   w_down  wdtype [E, d_pad, f_pad]  (= w_down^T per expert: row = output channel)
  * Experts 0..N-1 are routed, N..E-1 are the shared experts (weight 1.0, added
- * after the routed ones, beam.py:163-164). */
+ * after the routed ones, beam.py:163-164).
+ *   gate_w3 (optional, NULL = built per call) bf16 [3, gate_w3_cols, d_pad]: the
+ *           prefill tensor-core router's operand, (norm_w o gate_wT rows) split
+ *           into hi / mid / lo bf16 terms (beam_router_split), cached at pack time */
 typedef struct {
   int d_h, d_ff, num_experts, top_k, num_shared;
   int has_norm;
@@ -101,7 +104,15 @@ typedef struct {
   const float* gate_wT;
   const void* w_gu;
   const void* w_down;
+  const void* gate_w3;
+  int gate_w3_cols;
 } beam_layer_t;
+
+/* The three-term bf16 split of the (norm-weighted) projection rows for the
+ * prefill tensor-core router: out [3, cols, d_pad] bf16 (hi + mid + lo carry the
+ * 24 significant bits of norm_w[k] * gate_wT[c, k]); norm_w may be NULL. */
+int beam_router_split(const float* gate_wT, const float* norm_w, int cols, int d, int d_pad, void* out,
+                      beam_stream_t stream);
 
 /* Optional outputs of beam_layer_forward (any may be NULL except `out`). */
 typedef struct {
@@ -284,6 +295,9 @@ int beam_ep_combine(const float* y_back, const int32_t* send_pos, int world, int
  *  token 0: partials summed, top-K selected, softmax done, outputs stored}. */
 int beam_trace_gate(unsigned long long* dev_buf);
 const char* beam_last_cuda_error(void);
+/* sizeof the ABI structs (0 beam_layer_t, 1 beam_outputs_t, 2 beam_route_t): lets
+ * FFI bindings check their struct mirrors against the compiled library. */
+size_t beam_abi_sizeof(int which);
 const char* beam_build_info(void);
 /* 1 if `p` is page-locked host memory the GPU can address at the same pointer
  * (UVA-mapped), so kernels may write results straight into it (the host-output

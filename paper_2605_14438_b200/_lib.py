@@ -50,6 +50,8 @@ EXPORTS = (
     "beam_last_cuda_error",
     "beam_build_info",
     "beam_host_mapped",
+    "beam_router_split",
+    "beam_abi_sizeof",
     "beam_ep_tiles",
     "beam_ep_count",
     "beam_ep_pack",
@@ -80,6 +82,8 @@ class LayerDesc(ctypes.Structure):
         ("gate_wT", ctypes.c_void_p),
         ("w_gu", ctypes.c_void_p),
         ("w_down", ctypes.c_void_p),
+        ("gate_w3", ctypes.c_void_p),
+        ("gate_w3_cols", ctypes.c_int),
     ]
 
 
@@ -152,6 +156,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_last_cuda_error": (ctypes.c_char_p, []),
         "beam_build_info": (ctypes.c_char_p, []),
         "beam_host_mapped": (I, [P]),
+        "beam_router_split": (I, [P, P, I, I, I, P, P]),
+        "beam_abi_sizeof": (S, [I]),
         "beam_ep_tiles": (I, [I]),
         "beam_ep_count": (I, [P, I, I, I, I, P, P]),
         "beam_ep_pack": (I, [P, I, I, I, P, P, I, I, I, I, P, I, P, P, P, P, P]),

@@ -312,7 +312,8 @@ static cudaError_t run_gate(const beam_layer_t& L, const Dims& g, const void* X,
   cudaError_t e;
   int splits;
   if (w.rscratch && router_tc_supported(T, sp.cols, g.d_pad, h_dtype)) {
-    e = launch_router_tc(X, nw, L.gate_wT, T, sp.cols, g.d, g.d_pad, w.logits2, w.rscratch, s);
+    const void* w3 = (L.gate_w3 != nullptr && L.gate_w3_cols == sp.cols) ? L.gate_w3 : nullptr;
+    e = launch_router_tc(X, nw, L.gate_wT, w3, T, sp.cols, g.d, g.d_pad, w.logits2, w.rscratch, s);
     splits = router_tc_splits();
   } else {
     e = launch_router(X, h_dtype, nw, L.gate_wT, T, sp.cols, g.d, g.d_pad, w.logits2, s);
@@ -346,10 +347,18 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
   // weight-streaming expert kernels
   const bool prescaled = L.has_norm && w.xw != nullptr && !w.tc && gate_fused_supported(T, g.N, g.E, g.d_pad);
   if (gate_fused_supported(T, g.N, g.E, g.d_pad)) {
-    // decode: projection + top-K + permute in one launch
-    BEAM_TRY(launch_gate_fused(X, h_dtype, L.has_norm ? L.norm_w : nullptr, L.gate_wT, T, g.d, g.d_pad,
-                               w.logits2, topk_args(L, g, o, w, sp), g.E, block_size, w.tc, w.plan, w.counters, s,
-                               prescaled ? w.xw : nullptr));
+    // decode: projection + top-K + permute in one launch — on thread-block
+    // clusters (gate_cluster.cu) where the part schedules them, else the split-K
+    // fused gate (gate.cu)
+    const float* nw = L.has_norm ? L.norm_w : nullptr;
+    cudaError_t e = cudaErrorNotSupported;
+    if (gate_cluster_supported(T, sp.cols, sp.Nr, g.E, g.d_pad))
+      e = launch_gate_cluster(X, h_dtype, nw, L.gate_wT, T, g.d, g.d_pad, topk_args(L, g, o, w, sp), g.E,
+                              block_size, w.tc, w.plan, w.counters + 16, prescaled ? w.xw : nullptr, s);
+    if (e == cudaErrorNotSupported)
+      e = launch_gate_fused(X, h_dtype, nw, L.gate_wT, T, g.d, g.d_pad, w.logits2, topk_args(L, g, o, w, sp), g.E,
+                            block_size, w.tc, w.plan, w.counters, s, prescaled ? w.xw : nullptr);
+    BEAM_TRY(e);
     prof_mark(1, s);
   } else {
     BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s, sp));
@@ -680,6 +689,12 @@ int beam_trace_rows(const int64_t* topk_ids, const int64_t* masked_ids, const in
                                   active_count, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+int beam_router_split(const float* gate_wT, const float* norm_w, int cols, int d, int d_pad, void* out,
+                      beam_stream_t stream) {
+  if (!gate_wT || !out || cols < 1 || d < 1 || d_pad < d) return BEAM_ERR_ARG;
+  return status(launch_router_split(gate_wT, norm_w, cols, d, d_pad, out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int beam_rms_norm(const void* h, int h_dtype, int T, int d, const float* norm_w, float* out,
                   beam_stream_t stream) {
   if (T < 0 || d < 1) return BEAM_ERR_ARG;
@@ -733,6 +748,15 @@ int beam_profile_end(float* stage_ms, int* calls) {
 int beam_trace_gate(unsigned long long* dev_buf) { return status(beam::set_gate_trace(dev_buf)); }
 
 const char* beam_last_cuda_error(void) { return g_last_error; }
+
+size_t beam_abi_sizeof(int which) {
+  switch (which) {
+    case 0: return sizeof(beam_layer_t);
+    case 1: return sizeof(beam_outputs_t);
+    case 2: return sizeof(beam_route_t);
+    default: return 0;
+  }
+}
 
 int beam_host_mapped(const void* p) {
   cudaPointerAttributes a;

@@ -111,6 +111,13 @@ cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, c
                               int d, int d_pad, float* P, const TopkArgs& a, int E, int bs,
                               bool pad, const PlanDev& p, int* counters, cudaStream_t s,
                               float* xw = nullptr);  // xw: [T, d_pad] x * norm_w (fp32) when norm_w is set
+// gate_cluster.cu (decode gate on thread-block clusters; cudaErrorNotSupported
+// when the part cannot co-schedule a cluster: the caller falls back to the
+// fused gate)
+bool gate_cluster_supported(int T, int cols, int Nr, int E, int d_pad);
+cudaError_t launch_gate_cluster(const void* X, int x_dtype, const float* norm_w, const float* gate_wT, int T, int d,
+                                int d_pad, const TopkArgs& a, int E, int bs, bool pad, const PlanDev& p, int* counter,
+                                float* xw, cudaStream_t s);
 cudaError_t launch_mask_route(const int64_t* ids, const void* a, int a_dtype, int T, int K,
                               int N, int64_t* out, cudaStream_t s);
 cudaError_t launch_topk_select(const void* logits, int dtype, int T, int N, int K, int64_t* out, cudaStream_t s);
@@ -153,7 +160,9 @@ void set_gemm_variant(int v);  // 0 = 2-SM pairs when possible, 1 = 1-SM kernel
 bool router_tc_supported(int T, int cols, int d_pad, int x_dtype);
 size_t router_tc_scratch_bytes(int cols, int d_pad);
 int router_tc_splits();  // split-K partials the tensor-core router writes
-cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* gate_wT, int T, int cols, int d,
+cudaError_t launch_router_split(const float* gate_wT, const float* norm_w, int cols, int d, int d_pad, void* A3,
+                                cudaStream_t s);
+cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* gate_wT, const void* w3, int T, int cols, int d,
                              int d_pad, float* P, void* scratch, cudaStream_t s);
 // opair written as bf16 [cap, d_pad] (combine reads it with BEAM_BF16)
 cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* xperm, const PlanDev& p,

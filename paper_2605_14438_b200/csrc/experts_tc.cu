@@ -188,8 +188,8 @@ __device__ __forceinline__ Tile decode(int u, const int* tile_off, int E, int MG
   const int n_tile = local % nt;
   r.a_row0 = lo * a.m_rows + r.m_tile * BM;
   const int tok0 = n_tile * a.bn;
-  r.ntok = min(a.bn, a.counts[lo] - tok0);
-  r.b_row0 = a.offsets[lo] + tok0;
+  r.ntok = min(a.bn, (a.mode == 2 ? a.p_T : a.counts[lo]) - tok0);
+  r.b_row0 = (a.mode == 2 ? 0 : a.offsets[lo]) + tok0;
   r.nmma = (r.ntok + 15) & ~15;
   return r;
 }
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) tile_off[0] = 0;
     for (int base = 0; base < E; base += 32) {
       const int e = base + lane;
-      int v = e < E ? (args.counts[e] + args.bn - 1) / args.bn : 0;
+      int v = e < E ? ((args.mode == 2 ? args.p_T : args.counts[e]) + args.bn - 1) / args.bn : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, v, o);
@@ -544,7 +544,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     if (lane == 0) tile_off[0] = 0;
     for (int base = 0; base < E; base += 32) {
       const int e = base + lane;
-      int v = e < E ? (args.counts[e] + args.bn - 1) / args.bn : 0;
+      int v = e < E ? ((args.mode == 2 ? args.p_T : args.counts[e]) + args.bn - 1) / args.bn : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, v, o);
@@ -925,7 +925,7 @@ cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* 
 // (the tile count, not the FLOPs, bounds this small GEMM).
 // ---------------------------------------------------------------------------
 __global__ void split_router_kernel(const float* __restrict__ W, const float* __restrict__ nw, int cols, int d,
-                                    int d_pad, __nv_bfloat16* __restrict__ A3, int T, int32_t* __restrict__ plan1) {
+                                    int d_pad, __nv_bfloat16* __restrict__ A3) {
   const size_t n = (size_t)cols * d_pad;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int c = (int)(i / d_pad), k = (int)(i % d_pad);
@@ -939,10 +939,14 @@ __global__ void split_router_kernel(const float* __restrict__ W, const float* __
     A3[((size_t)cols + c) * d_pad + k] = mid;
     A3[((size_t)2 * cols + c) * d_pad + k] = lo;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    plan1[0] = T;  // counts[0]
-    plan1[1] = 0;  // offsets[0]
-  }
+}
+
+cudaError_t launch_router_split(const float* gate_wT, const float* norm_w, int cols, int d, int d_pad, void* A3,
+                                cudaStream_t s) {
+  split_router_kernel<<<std::min(4096, (int)(((size_t)cols * d_pad + 255) / 256)), 256, 0, s>>>(
+      gate_wT, norm_w, cols, d, d_pad, reinterpret_cast<__nv_bfloat16*>(A3));
+  count_launches(1);
+  return cudaGetLastError();
 }
 
 bool router_tc_supported(int T, int cols, int d_pad, int x_dtype) {
@@ -953,24 +957,26 @@ size_t router_tc_scratch_bytes(int cols, int d_pad) { return (size_t)cols * 3 * 
 
 int router_tc_splits() { return 3; }
 
-cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* gate_wT, int T, int cols, int d,
-                             int d_pad, float* P, void* scratch, cudaStream_t s) {
+// w3: the cached split (beam_layer_t.gate_w3) or NULL (split into `scratch` here)
+cudaError_t launch_router_tc(const void* X, const float* norm_w, const float* gate_wT, const void* w3, int T, int cols,
+                             int d, int d_pad, float* P, void* scratch, cudaStream_t s) {
   using namespace tc;
-  __nv_bfloat16* A3 = reinterpret_cast<__nv_bfloat16*>(scratch);
-  int32_t* plan1 = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(scratch) + (size_t)cols * 3 * d_pad * 2);
-  split_router_kernel<<<std::min(4096, (int)(((size_t)cols * d_pad + 255) / 256)), 256, 0, s>>>(
-      gate_wT, norm_w, cols, d, d_pad, A3, T, plan1);
-  count_launches(1);
+  const void* A3 = w3;
+  if (A3 == nullptr) {
+    cudaError_t e = launch_router_split(gate_wT, norm_w, cols, d, d_pad, scratch, s);
+    if (e != cudaSuccess) return e;
+    A3 = scratch;
+  }
   CUtensorMap mA, mB;
   if (!make_map(&mA, A3, 3ull * cols, d_pad, BM) || !make_map(&mB, X, (uint64_t)T, d_pad, kBBox))
     return cudaErrorInvalidValue;
-  // one "expert" of T tokens: narrow the token tiles until the units cover the SMs
+  // one "expert" of T tokens (count taken from p_T: no device-side plan)
   static const int env_bn = [] {
     const char* v = getenv("BEAM_ROUTER_BN");  // tuning knob
     return v ? atoi(v) : 0;
   }();
   int bn = env_bn >= 16 && env_bn <= BN && env_bn % 16 == 0 ? env_bn : BN;
-  Args a{2, 1, 3 * cols, d_pad, d_pad / BK, plan1, plan1 + 1, nullptr, nullptr, 0, P, 0, bn, cols, T};
+  Args a{2, 1, 3 * cols, d_pad, d_pad / BK, nullptr, nullptr, nullptr, nullptr, 0, P, 0, bn, cols, T};
   return launch_gemm(mA, mB, a, smem_bytes(1), true, s);
 }
 

@@ -47,91 +47,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// One warp, one token.  L = projection partials [splits][T][a.cols]: router
-// logits in columns [0, Nr), mask pre-activations (if any) in [mask_off,
-// mask_off + N); X = the token rows (stride d_pad) for inv_rms.  NPL = ceil(Nr / 32).
-// a.kind selects the routing rule (baselines.py:158-283, inference branch):
-//   BEAM     keep iff a >= thr, ghat = g * m                    (beam.py:127-165)
-//   TOPK     keep every candidate (vanilla / reduced / pruning: K = k_eff)
-//   DYNAMIC  p = softmax over all N; keep the shortest descending prefix with
-//            mass >= phi (dynamic_select, baselines.py:132-143); ghat = p / mass
-//   ADA      top-K over N real + null columns, keep the real ones, ghat = g
-//   SOFT     s = sigmoid(a / temp); binarize: keep iff s >= tau, ghat = g * keep;
-//            else keep all, ghat = g * s
-// KIND >= 0 fixes the rule at compile time (the BEAM hot path carries none of
-// the other rules' code); KIND = -1 reads a.kind.
-template <typename TX, int NPL, int MAXSPLIT, bool CG, int KIND = -1>
-__device__ __forceinline__ void topk_token(const float* __restrict__ L, int splits, int T,
-                                           const TX* __restrict__ X, int t, int lane,
-                                           const TopkArgs& a) {
+// The selection half of topk_token, on one token's router logits v / mask
+// pre-activations av (lane's columns j = lane + 32 i, NOT yet scaled by the
+// token's inv_rms): top-K, softmax over the K kept logits, the routing rule,
+// and every output of the token.  Shared by the split-K top-K kernels and the
+// cluster gate (which gathers v / av from distributed shared memory).
+template <int NPL, int KIND = -1>
+__device__ __forceinline__ void topk_finish(float (&v)[NPL], float (&av)[NPL], float inv, int t, int lane,
+                                            const TopkArgs& a) {
   const int N = a.N, Nr = KIND == BEAM_ROUTE_BEAM ? a.N : a.Nr, K = a.K, Keff = a.K + a.S;
   const int kind = KIND >= 0 ? KIND : a.kind;
-  float inv = 1.0f;
-  if (a.has_norm && a.ss_part != nullptr) {  // split partials from the projection CTAs
-    float ss = 0.0f;
-#pragma unroll
-    for (int sp = 0; sp < MAXSPLIT; ++sp) {
-      const float v = ld_maybe_cg<CG>(a.ss_part + (size_t)min(sp, splits - 1) * T + t);
-      ss += sp < splits ? v : 0.0f;
-    }
-    inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
-  } else if (a.has_norm) {  // tensor.py:485-487: (mean(x^2) + eps)^-1/2 over the real d entries
-    const TX* row = X + (size_t)t * a.d_pad;
-    float ss = 0.0f;
-#pragma unroll 8
-    for (int k = 4 * lane; k < a.d_pad; k += 128) {
-      const float4 x = ld4<TX>(row + k);
-      ss = fmaf(x.x, x.x, ss);
-      ss = fmaf(x.y, x.y, ss);
-      ss = fmaf(x.z, x.z, ss);
-      ss = fmaf(x.w, x.w, ss);
-    }
-    ss = warp_sum(ss);
-    inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
-  }
-  if (a.inv_out && lane == 0) a.inv_out[t] = inv;
-
-  // router logits v / mask pre-activations av of this lane's columns j = lane + 32 i,
-  // summed over the split-K partials in split order
-  float v[NPL], av[NPL];
+  const bool has_mask = KIND == BEAM_ROUTE_BEAM ? true : a.mask_off >= 0;
   int rank[NPL];
 #pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    v[i] = 0.0f;
-    av[i] = 0.0f;
-    rank[i] = -1;
-  }
-  const bool has_mask = KIND == BEAM_ROUTE_BEAM ? true : a.mask_off >= 0;
-  const int cols = KIND == BEAM_ROUTE_BEAM ? 2 * a.N : a.cols;
-  const int mask_off = KIND == BEAM_ROUTE_BEAM ? a.N : a.mask_off;
-  // Loads are unconditional (clamped split / column index, masked add) and issued
-  // four splits at a time: conditional loads inside the unrolled loop would be
-  // serialised, one L2 round trip each.  The sum runs in split order.
-  constexpr int kSB = MAXSPLIT < 4 ? MAXSPLIT : 4;
-#pragma unroll
-  for (int sp0 = 0; sp0 < MAXSPLIT; sp0 += kSB) {
-    if (sp0 < splits) {
-      float pv[kSB][NPL], pa[kSB][NPL];
-#pragma unroll
-      for (int q = 0; q < kSB; ++q) {
-        const float* row = L + ((size_t)min(sp0 + q, splits - 1) * T + t) * cols;
-#pragma unroll
-        for (int i = 0; i < NPL; ++i) {
-          pv[q][i] = ld_maybe_cg<CG>(row + min(lane + 32 * i, Nr - 1));
-          pa[q][i] = has_mask ? ld_maybe_cg<CG>(row + mask_off + min(lane + 32 * i, N - 1)) : 0.0f;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < kSB; ++q)
-#pragma unroll
-        for (int i = 0; i < NPL; ++i) {
-          if (sp0 + q < splits) {
-            v[i] += pv[q][i];
-            av[i] += pa[q][i];
-          }
-        }
-    }
-  }
+  for (int i = 0; i < NPL; ++i) rank[i] = -1;
 #pragma unroll
   for (int i = 0; i < NPL; ++i) {
     v[i] *= inv;
@@ -292,6 +221,92 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
       a.gw_s[o] = 1.0f;
     }
   }
+}
+
+
+// One warp, one token.  L = projection partials [splits][T][a.cols]: router
+// logits in columns [0, Nr), mask pre-activations (if any) in [mask_off,
+// mask_off + N); X = the token rows (stride d_pad) for inv_rms.  NPL = ceil(Nr / 32).
+// a.kind selects the routing rule (baselines.py:158-283, inference branch):
+//   BEAM     keep iff a >= thr, ghat = g * m                    (beam.py:127-165)
+//   TOPK     keep every candidate (vanilla / reduced / pruning: K = k_eff)
+//   DYNAMIC  p = softmax over all N; keep the shortest descending prefix with
+//            mass >= phi (dynamic_select, baselines.py:132-143); ghat = p / mass
+//   ADA      top-K over N real + null columns, keep the real ones, ghat = g
+//   SOFT     s = sigmoid(a / temp); binarize: keep iff s >= tau, ghat = g * keep;
+//            else keep all, ghat = g * s
+// KIND >= 0 fixes the rule at compile time (the BEAM hot path carries none of
+// the other rules' code); KIND = -1 reads a.kind.
+template <typename TX, int NPL, int MAXSPLIT, bool CG, int KIND = -1>
+__device__ __forceinline__ void topk_token(const float* __restrict__ L, int splits, int T,
+                                           const TX* __restrict__ X, int t, int lane,
+                                           const TopkArgs& a) {
+  const int N = a.N, Nr = KIND == BEAM_ROUTE_BEAM ? a.N : a.Nr;
+  float inv = 1.0f;
+  if (a.has_norm && a.ss_part != nullptr) {  // split partials from the projection CTAs
+    float ss = 0.0f;
+#pragma unroll
+    for (int sp = 0; sp < MAXSPLIT; ++sp) {
+      const float v = ld_maybe_cg<CG>(a.ss_part + (size_t)min(sp, splits - 1) * T + t);
+      ss += sp < splits ? v : 0.0f;
+    }
+    inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
+  } else if (a.has_norm) {  // tensor.py:485-487: (mean(x^2) + eps)^-1/2 over the real d entries
+    const TX* row = X + (size_t)t * a.d_pad;
+    float ss = 0.0f;
+#pragma unroll 8
+    for (int k = 4 * lane; k < a.d_pad; k += 128) {
+      const float4 x = ld4<TX>(row + k);
+      ss = fmaf(x.x, x.x, ss);
+      ss = fmaf(x.y, x.y, ss);
+      ss = fmaf(x.z, x.z, ss);
+      ss = fmaf(x.w, x.w, ss);
+    }
+    ss = warp_sum(ss);
+    inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
+  }
+  if (a.inv_out && lane == 0) a.inv_out[t] = inv;
+
+  // router logits v / mask pre-activations av of this lane's columns j = lane + 32 i,
+  // summed over the split-K partials in split order
+  float v[NPL], av[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    v[i] = 0.0f;
+    av[i] = 0.0f;
+  }
+  const bool has_mask = KIND == BEAM_ROUTE_BEAM ? true : a.mask_off >= 0;
+  const int cols = KIND == BEAM_ROUTE_BEAM ? 2 * a.N : a.cols;
+  const int mask_off = KIND == BEAM_ROUTE_BEAM ? a.N : a.mask_off;
+  // Loads are unconditional (clamped split / column index, masked add) and issued
+  // four splits at a time: conditional loads inside the unrolled loop would be
+  // serialised, one L2 round trip each.  The sum runs in split order.
+  constexpr int kSB = MAXSPLIT < 4 ? MAXSPLIT : 4;
+#pragma unroll
+  for (int sp0 = 0; sp0 < MAXSPLIT; sp0 += kSB) {
+    if (sp0 < splits) {
+      float pv[kSB][NPL], pa[kSB][NPL];
+#pragma unroll
+      for (int q = 0; q < kSB; ++q) {
+        const float* row = L + ((size_t)min(sp0 + q, splits - 1) * T + t) * cols;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) {
+          pv[q][i] = ld_maybe_cg<CG>(row + min(lane + 32 * i, Nr - 1));
+          pa[q][i] = has_mask ? ld_maybe_cg<CG>(row + mask_off + min(lane + 32 * i, N - 1)) : 0.0f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kSB; ++q)
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) {
+          if (sp0 + q < splits) {
+            v[i] += pv[q][i];
+            av[i] += pa[q][i];
+          }
+        }
+    }
+  }
+  topk_finish<NPL, KIND>(v, av, inv, t, lane, a);
 }
 
 // Block-wide exclusive scan of one int per thread (NW warps, NW <= 32).

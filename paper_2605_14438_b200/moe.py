@@ -355,8 +355,18 @@ class MoEBlock:
                 if nr > cfg.num_experts:
                     raise ContractError("a block with null-expert router columns has no mask router")
                 gate[cfg.num_experts : 2 * cfg.num_experts, : cfg.d_h] = mw.t()
+            # the prefill tensor-core router's bf16 hi/mid/lo split of (norm_w o gate rows),
+            # built once here instead of on every prefill call
+            rows = gate.shape[0]
+            if getattr(self, "gate_w3", None) is None or self.gate_w3.shape[1] != rows:
+                self.gate_w3 = torch.empty(3, rows, cfg.d_pad, dtype=torch.bfloat16, device=self.device)
+            if self.device.type == "cuda":
+                _lib.check(_lib.load().beam_router_split(
+                    gate.data_ptr(), self.norm_w.data_ptr() if self.norm_w is not None else None, rows, cfg.d_h,
+                    cfg.d_pad, self.gate_w3.data_ptr(), _runtime.stream_handle(self.device)), "beam_router_split")
             self._pack_key = key
-        ck = (key, mask_threshold, id(self.norm_w), id(self.w_gu), id(self.w_down), id(self.gate_wT))
+        ck = (key, mask_threshold, id(self.norm_w), id(self.w_gu), id(self.w_down), id(self.gate_wT),
+              id(getattr(self, "gate_w3", None)))
         cached = getattr(self, "_desc_cache", None)
         if cached is not None and cached[0] == ck:
             return cached[1]
@@ -371,6 +381,9 @@ class MoEBlock:
         d.gate_wT = self.gate_wT.data_ptr()
         d.w_gu = self.w_gu.data_ptr()
         d.w_down = self.w_down.data_ptr()
+        if self.device.type == "cuda":
+            d.gate_w3 = self.gate_w3.data_ptr()
+            d.gate_w3_cols = self.gate_w3.shape[1]
         self._desc_cache = (ck, d)
         return d
 

@@ -59,8 +59,13 @@ def test_struct_layout_matches_header(lib_path):
 
     from paper_2605_14438_b200 import _lib
 
-    # 9 x 4-byte fields (8 int + 1 float), then 4 pointers
-    assert ctypes.sizeof(_lib.LayerDesc) == 9 * 4 + 4 + 4 * 8
+    # the ctypes mirrors have the compiled structs' sizes (beam_abi_sizeof)
+    lib = _lib.load(lib_path)
+    assert ctypes.sizeof(_lib.LayerDesc) == lib.beam_abi_sizeof(0)
+    assert ctypes.sizeof(_lib.Outputs) == lib.beam_abi_sizeof(1)
+    assert ctypes.sizeof(_lib.RouteDesc) == lib.beam_abi_sizeof(2)
+    # 9 x 4-byte fields (8 int + 1 float), 4 pad, 5 pointers, the split's column count (+ pad)
+    assert ctypes.sizeof(_lib.LayerDesc) == 9 * 4 + 4 + 5 * 8 + 8
     assert ctypes.sizeof(_lib.Outputs) == 9 * 8  # 8 output pointers + decision_event
 
 

@@ -45,7 +45,20 @@ def _port():
     return p
 
 
+_BLOCKS = {}
+
+
 def _q30_block(seed, has_norm=True):
+    """(oracle block, GPU block) of the Qwen3-30B shape, cached per seed (the
+    numpy draw of 604 M expert weights dominates a test's time)."""
+    key = (seed, has_norm)
+    if key not in _BLOCKS:
+        _BLOCKS.clear()
+        _BLOCKS[key] = _make_q30_block(seed, has_norm)
+    return _BLOCKS[key]
+
+
+def _make_q30_block(seed, has_norm):
     rng = np.random.default_rng(seed)
     ob = O.make_block(2048, 768, 128, 8, rng, init_std=0.02, has_norm=has_norm)
     ob.mask_w = rng.normal(0, 1 / np.sqrt(2048), (2048, 128))
@@ -109,9 +122,9 @@ def test_pack_kernel_matches_host_restatement(world, cap):
                                       ((300, 512, 130, 0, 260, 700, 64, 300), False)])
 @pytest.mark.parametrize("h_dtype", [torch.bfloat16, torch.float32])
 def test_virtual_ep_matches_single_gpu(world, ts, fixed, h_dtype):
-    ob, gb = _q30_block(60 + world)
+    ob, gb = _q30_block(60)
     layers = [EPBeamLayer.from_block(gb, rank=r, world=world) for r in range(world)]
-    rng = np.random.default_rng(world)
+    rng = np.random.default_rng(world + 10 * len(ts))
     hs = [torch.from_numpy(rng.normal(size=(ts[r % len(ts)], 2048))).to(h_dtype).cuda() for r in range(world)]
     outs = virtual_forward(layers, hs, fixed=fixed)
     for h, o in zip(hs, outs):
@@ -179,7 +192,7 @@ def nccl_group():
 
 @pytest.mark.parametrize("t,capacity", [(1, None), (64, 64), (300, None)])
 def test_ep_single_rank_nccl_matches_layer(nccl_group, t, capacity):
-    ob, gb = _q30_block(40 + t)
+    ob, gb = _q30_block(60)
     x = torch.from_numpy(np.random.default_rng(t).normal(size=(t, 2048))).to(torch.bfloat16).cuda()
     ep = EPBeamLayer.from_block(gb, capacity=capacity)
     out_ep = ep.forward(x)
