@@ -175,6 +175,22 @@ static int validate(const beam_layer_t* L) {
 
 static int status(cudaError_t e) { return record(e) == cudaSuccess ? BEAM_OK : BEAM_ERR_CUDA; }
 
+// Decode gate: the fused single-launch gate (gate.cu: projection + top-K +
+// permute with last-CTA handoffs) for T <= kFusedGateMaxT; above, three launches
+// (split-K projection, top-K, permute) are as fast or faster (B200, L2 flushed,
+// Q30 layer: T=1 51.1 vs 53.4 us, T=8 115.0 vs 111.8 us, T=64 223.8 vs 223.0 us;
+// profiles/r02/gate_modes.jsonl).  BEAM_GATE_MODE=fused|split forces one
+// (diagnostics).
+constexpr int kFusedGateMaxT = 4;
+static bool use_fused_gate(int T) {
+  static const int m = [] {
+    const char* v = getenv("BEAM_GATE_MODE");
+    if (v == nullptr) return 0;
+    return v[0] == 'f' ? 1 : v[0] == 's' ? 2 : 0;
+  }();
+  return m == 1 || (m == 0 && T <= kFusedGateMaxT);
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* v = getenv("BEAM_NO_PDL");
@@ -346,19 +362,11 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
   // decode with an RMS norm: the fused gate also writes x * norm_w (fp32) for the
   // weight-streaming expert kernels
   const bool prescaled = L.has_norm && w.xw != nullptr && !w.tc && gate_fused_supported(T, g.N, g.E, g.d_pad);
-  if (gate_fused_supported(T, g.N, g.E, g.d_pad)) {
-    // decode: projection + top-K + permute in one launch — on thread-block
-    // clusters (gate_cluster.cu) where the part schedules them, else the split-K
-    // fused gate (gate.cu)
-    const float* nw = L.has_norm ? L.norm_w : nullptr;
-    cudaError_t e = cudaErrorNotSupported;
-    if (gate_cluster_supported(T, sp.cols, sp.Nr, g.E, g.d_pad))
-      e = launch_gate_cluster(X, h_dtype, nw, L.gate_wT, T, g.d, g.d_pad, topk_args(L, g, o, w, sp), g.E,
-                              block_size, w.tc, w.plan, w.counters + 16, prescaled ? w.xw : nullptr, s);
-    if (e == cudaErrorNotSupported)
-      e = launch_gate_fused(X, h_dtype, nw, L.gate_wT, T, g.d, g.d_pad, w.logits2, topk_args(L, g, o, w, sp), g.E,
-                            block_size, w.tc, w.plan, w.counters, s, prescaled ? w.xw : nullptr);
-    BEAM_TRY(e);
+  if (use_fused_gate(T) && gate_fused_supported(T, g.N, g.E, g.d_pad)) {
+    // small decode batches: projection + top-K + permute in one launch
+    BEAM_TRY(launch_gate_fused(X, h_dtype, L.has_norm ? L.norm_w : nullptr, L.gate_wT, T, g.d, g.d_pad,
+                               w.logits2, topk_args(L, g, o, w, sp), g.E, block_size, w.tc, w.plan, w.counters, s,
+                               prescaled ? w.xw : nullptr));
     prof_mark(1, s);
   } else {
     BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s, sp));

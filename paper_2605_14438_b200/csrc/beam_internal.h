@@ -111,13 +111,6 @@ cudaError_t launch_gate_fused(const void* X, int x_dtype, const float* norm_w, c
                               int d, int d_pad, float* P, const TopkArgs& a, int E, int bs,
                               bool pad, const PlanDev& p, int* counters, cudaStream_t s,
                               float* xw = nullptr);  // xw: [T, d_pad] x * norm_w (fp32) when norm_w is set
-// gate_cluster.cu (decode gate on thread-block clusters; cudaErrorNotSupported
-// when the part cannot co-schedule a cluster: the caller falls back to the
-// fused gate)
-bool gate_cluster_supported(int T, int cols, int Nr, int E, int d_pad);
-cudaError_t launch_gate_cluster(const void* X, int x_dtype, const float* norm_w, const float* gate_wT, int T, int d,
-                                int d_pad, const TopkArgs& a, int E, int bs, bool pad, const PlanDev& p, int* counter,
-                                float* xw, cudaStream_t s);
 cudaError_t launch_mask_route(const int64_t* ids, const void* a, int a_dtype, int T, int K,
                               int N, int64_t* out, cudaStream_t s);
 cudaError_t launch_topk_select(const void* logits, int dtype, int T, int N, int K, int64_t* out, cudaStream_t s);

@@ -183,9 +183,26 @@ __device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const
   const int nt = min(TT, T - t0);
   const int ks = split * kr, ke = min(d_pad, ks + kr);
   const int kn = ke - ks;
-  for (int v = threadIdx.x; v < nt * (kn >> 2); v += 256) {
-    const int t = v / (kn >> 2), k4 = v % (kn >> 2);
-    *reinterpret_cast<float4*>(xs + t * kr + 4 * k4) = ld4<TX>(X + (size_t)(t0 + t) * d_pad + ks + 4 * k4);
+  {
+    // token tile -> shared memory, loads batched U deep (each iteration's load
+    // would otherwise wait a full memory round trip before the next is issued)
+    constexpr int U = 4;
+    const int n4 = nt * (kn >> 2);
+    for (int v0 = threadIdx.x; v0 < n4; v0 += 256 * U) {
+      float4 xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + 256 * u;
+        const int t = v / (kn >> 2), k4 = v % (kn >> 2);
+        xv[u] = v < n4 ? ld4<TX>(X + (size_t)(t0 + t) * d_pad + ks + 4 * k4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + 256 * u;
+        const int t = v / (kn >> 2), k4 = v % (kn >> 2);
+        if (v < n4) *reinterpret_cast<float4*>(xs + t * kr + 4 * k4) = xv[u];
+      }
+    }
   }
   float4 wa[kGemvSteps], wb[kGemvSteps];
   const float* w0 = W + (size_t)min(c0, cols - 1) * d_pad;

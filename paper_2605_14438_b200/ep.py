@@ -262,10 +262,12 @@ class EPBeamLayer:
         if not self._staged:
             dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
             return
-        wire = {2: torch.int16, 4: torch.int32, 8: torch.int64}[inp.element_size()]
-        o = torch.empty(out.shape, dtype=out.dtype).view(wire)
-        dist.all_to_all_single(o, inp.cpu().view(wire), out_splits, in_splits, group=self.group)
-        out.copy_(o.view(out.dtype))
+        # gloo + CUDA tensors: through host memory, as raw bytes (gloo has no
+        # bf16 / int16 all-to-all); rows stay dim 0, so the splits are unchanged
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(o.view(torch.uint8), inp.cpu().contiguous().view(torch.uint8), out_splits, in_splits,
+                               group=self.group)
+        out.copy_(o)
 
     def _protocol(self, t: int):
         """(cap, fixed): the same on every rank."""

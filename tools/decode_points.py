@@ -60,7 +60,7 @@ def main():
             stages = {nm: round(st[i] * 1e3 / max(nc.value, 1), 2) for i, nm in enumerate(names)}
             print(json.dumps({"shape": args.shape, "T": t, "s": s, "s_real": round(p["s_real"], 4),
                               "E_act": p["e_act"], "us": round(p["ms"] * 1e3, 2), "stages_eager_us": stages,
-                              "gate_cluster": os.environ.get("BEAM_GATE_CLUSTER", "1")}), flush=True)
+                              "gate_mode": os.environ.get("BEAM_GATE_MODE", "auto")}), flush=True)
             del p, layer
 
 

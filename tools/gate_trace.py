@@ -1,16 +1,23 @@
-"""Phase timeline of the fused decode gate (beam_trace_gate) at the bench's
-Q30 decode shapes, L2 flushed before every call (as in bench.py)."""
+"""Phase timeline of the fused decode gate (beam_trace_gate) at the bench's Q30
+decode shapes (BEAM_GATE_MODE=fused forces it at every T).  Medians over calls,
+microseconds from the first CTA's entry; L2 flushed before every call (as in
+bench.py) and not.  (Round 2 also traced a thread-block-cluster gate here —
+profiles/r02/gate_traces.log — measured slower and removed.)"""
 import ctypes
+import os
+import sys
 
 import numpy as np
 import torch
 
-import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import bench
-import paper_2605_14438_b200 as B
-from paper_2605_14438_b200 import _lib
-from paper_2605_14438_b200.beam import LayerOutputs, layer_forward_into
+import bench  # noqa: E402
+import paper_2605_14438_b200 as B  # noqa: E402
+from paper_2605_14438_b200 import _lib  # noqa: E402
+from paper_2605_14438_b200.beam import LayerOutputs, layer_forward_into  # noqa: E402
+
+FUSED = ["start_skew", "proj_first", "proj_last", "topk_start", "t0_loaded", "t0_selected", "t0_softmax",
+         "t0_stored", "topk_done", "permute_start", "permute_done"]
 
 
 def main(flush_l2=True):
@@ -23,8 +30,6 @@ def main(flush_l2=True):
     lib = _lib.load()
     tr = torch.zeros(16, dtype=torch.int64, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    names = ["start_skew", "proj_first", "proj_last", "topk_start", "t0_loaded", "t0_selected", "t0_softmax",
-             "t0_stored", "topk_done", "permute_start", "permute_done"]
     for t in (1, 8, 64):
         hc = bench.make_tokens(t, 7)
         theta = bench.calibrate_theta(hc, w["router"], w["mask"], Q["k"], 0.5)
@@ -48,7 +53,8 @@ def main(flush_l2=True):
                 rows.append([v[1] - v[0], v[2] - v[0], v[3] - v[0], v[6] - v[0], v[8] - v[0], v[9] - v[0],
                              v[10] - v[0], v[11] - v[0], v[4] - v[0], v[7] - v[0], v[5] - v[0]])
         med = np.median(np.array(rows), axis=0) / 1e3
-        print(f"T={t} flush={flush_l2}: " + ", ".join(f"{n}={x:.2f}us" for n, x in zip(names, med)))
+        print(f"T={t} flush={flush_l2} fused: " + ", ".join(f"{n}={x:.2f}us" for n, x in zip(FUSED, med)),
+              flush=True)
 
 
 if __name__ == "__main__":
