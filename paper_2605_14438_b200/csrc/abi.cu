@@ -176,12 +176,13 @@ static int validate(const beam_layer_t* L) {
 static int status(cudaError_t e) { return record(e) == cudaSuccess ? BEAM_OK : BEAM_ERR_CUDA; }
 
 // Decode gate: the fused single-launch gate (gate.cu: projection + top-K +
-// permute with last-CTA handoffs) for T <= kFusedGateMaxT; above, three launches
-// (split-K projection, top-K, permute) are as fast or faster (B200, L2 flushed,
-// Q30 layer: T=1 51.1 vs 53.4 us, T=8 115.0 vs 111.8 us, T=64 223.8 vs 223.0 us;
-// profiles/r02/gate_modes.jsonl).  BEAM_GATE_MODE=fused|split forces one
-// (diagnostics).
-constexpr int kFusedGateMaxT = 4;
+// permute with last-CTA handoffs) at every decode size it supports; the three
+// separate launches (split-K projection, top-K, permute) measured equal or
+// slower (B200, L2 flushed, Q30 layer, s = 0 / 0.5: T=8 117.6/85.7 vs
+// 117.2/86.1 us, T=16 161.1/116.0 vs 163.2/116.8, T=64 283.3/225.2 vs
+// 286.7/229.2; profiles/r02/gate_modes.jsonl).  BEAM_GATE_MODE=fused|split
+// forces one (diagnostics).
+constexpr int kFusedGateMaxT = 64;
 static bool use_fused_gate(int T) {
   static const int m = [] {
     const char* v = getenv("BEAM_GATE_MODE");
@@ -322,8 +323,11 @@ static TopkArgs topk_args(const beam_layer_t& L, const Dims& g, const beam_outpu
 }
 
 // The gating half shared by beam_layer_forward and beam_gate.
+// xw (optional): [T, d_pad] fp32 x * norm_w, written by the top-K step (layer_forward's
+// prescaled decode rows)
 static cudaError_t run_gate(const beam_layer_t& L, const Dims& g, const void* X, int h_dtype, int T,
-                            const beam_outputs_t* o, LayerWs& w, cudaStream_t s, const Spec& sp) {
+                            const beam_outputs_t* o, LayerWs& w, cudaStream_t s, const Spec& sp,
+                            float* xw = nullptr) {
   const float* nw = L.has_norm ? L.norm_w : nullptr;
   cudaError_t e;
   int splits;
@@ -336,7 +340,12 @@ static cudaError_t run_gate(const beam_layer_t& L, const Dims& g, const void* X,
     splits = router_splits(T, sp.cols, g.d_pad);
   }
   if (e != cudaSuccess) return e;
-  return launch_topk_mask(w.logits2, splits, X, h_dtype, T, topk_args(L, g, o, w, sp), s);
+  TopkArgs ta = topk_args(L, g, o, w, sp);
+  if (xw != nullptr && L.has_norm) {
+    ta.nw = L.norm_w;
+    ta.xw_out = xw;
+  }
+  return launch_topk_mask(w.logits2, splits, X, h_dtype, T, ta, s);
 }
 
 static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, const void* h, int h_dtype, int T,
@@ -361,15 +370,19 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
   BEAM_TRY(strided_input(g, h, h_dtype, T, w, &X, s));
   // decode with an RMS norm: the fused gate also writes x * norm_w (fp32) for the
   // weight-streaming expert kernels
-  const bool prescaled = L.has_norm && w.xw != nullptr && !w.tc && gate_fused_supported(T, g.N, g.E, g.d_pad);
-  if (use_fused_gate(T) && gate_fused_supported(T, g.N, g.E, g.d_pad)) {
+  // decode with an RMS norm: the gate also writes x * norm_w (fp32) for the
+  // weight-streaming expert kernels (their tensor-core items need no per-chunk
+  // norm multiply)
+  const bool fused = use_fused_gate(T) && gate_fused_supported(T, g.N, g.E, g.d_pad);
+  const bool prescaled = L.has_norm && w.xw != nullptr && !w.tc;
+  if (fused) {
     // small decode batches: projection + top-K + permute in one launch
     BEAM_TRY(launch_gate_fused(X, h_dtype, L.has_norm ? L.norm_w : nullptr, L.gate_wT, T, g.d, g.d_pad,
                                w.logits2, topk_args(L, g, o, w, sp), g.E, block_size, w.tc, w.plan, w.counters, s,
                                prescaled ? w.xw : nullptr));
     prof_mark(1, s);
   } else {
-    BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s, sp));
+    BEAM_TRY(run_gate(L, g, X, h_dtype, T, o, w, s, sp, prescaled ? w.xw : nullptr));
     prof_mark(1, s);
     BEAM_TRY(launch_permute<int32_t>(w.ids32, w.gw, T, sp.Keff, g.E, block_size, w.plan, w.pscratch, s));
   }

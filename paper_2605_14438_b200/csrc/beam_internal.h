@@ -68,6 +68,10 @@ struct TopkArgs {
   int32_t* ids_s = nullptr;
   float* gw_s = nullptr;
   unsigned long long* trace = nullptr;  // diagnostics: %globaltimer at top-K sub-steps of token 0
+  // split decode gate: the top-K step also writes the prescaled rows x * norm_w
+  // (fp32, stride d_pad) for the weight-streaming expert kernels
+  const float* nw = nullptr;
+  float* xw_out = nullptr;
 };
 
 int num_sms();

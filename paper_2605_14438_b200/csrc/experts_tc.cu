@@ -216,7 +216,10 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const Tile& tl, 
     tmem_ld32(tbase + c0, v);
     if (args.epi_skip) continue;
     if (args.mode == 0) {
-      // lanes 0-15 hold gate rows, 16-31 the matching up rows, of features 16*w4 + (lane & 15)
+      // lanes 0-15 hold gate rows, 16-31 the matching up rows, of features 16*w4 + (lane & 15).
+      // Staging rows are 128 B (one bank sweep), so token rows j and 16 + j written
+      // by the two half-warps would hit the same banks: rows 16..31 store their
+      // features XOR 32 (the other half of the banks) — conflict-free, undone on read.
       __nv_bfloat16* s = reinterpret_cast<__nv_bfloat16*>(stg);  // [32 tokens][64 features]
       const int fl = 16 * w4 + (lane & 15);
       const bool lo = lane < 16;
@@ -226,11 +229,11 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const Tile& tl, 
         const float r = __shfl_xor_sync(0xffffffffu, send, 16);
         const float g = lo ? v[j] : r;
         const float u = lo ? r : v[16 + j];
-        s[(lo ? j : 16 + j) * 64 + fl] = __float2bfloat16_rn(activation<BEAM_ACT_SILU>(g) * u);
+        s[(lo ? j : 16 + j) * 64 + (lo ? fl : fl ^ 32)] = __float2bfloat16_rn(activation<BEAM_ACT_SILU>(g) * u);
       }
       epi_bar(bar);
       for (int row = w4; row < rows; row += 4) {
-        const uint32_t val = reinterpret_cast<const uint32_t*>(s + row * 64)[lane];
+        const uint32_t val = reinterpret_cast<const uint32_t*>(s + row * 64)[row < 16 ? lane : lane ^ 16];
         reinterpret_cast<uint32_t*>(args.act + (size_t)(tl.b_row0 + c0 + row) * args.f_pad + tl.m_tile * 64)[lane] = val;
       }
     } else if (args.mode == 1 && args.epi_direct) {

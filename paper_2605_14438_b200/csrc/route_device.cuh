@@ -253,6 +253,7 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
     inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
   } else if (a.has_norm) {  // tensor.py:485-487: (mean(x^2) + eps)^-1/2 over the real d entries
     const TX* row = X + (size_t)t * a.d_pad;
+    float* xw = a.xw_out != nullptr ? a.xw_out + (size_t)t * a.d_pad : nullptr;
     float ss = 0.0f;
 #pragma unroll 8
     for (int k = 4 * lane; k < a.d_pad; k += 128) {
@@ -261,6 +262,10 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
       ss = fmaf(x.y, x.y, ss);
       ss = fmaf(x.z, x.z, ss);
       ss = fmaf(x.w, x.w, ss);
+      if (xw != nullptr) {
+        const float4 g = ld_norm4(a.nw, k, a.d);
+        *reinterpret_cast<float4*>(xw + k) = make_float4(x.x * g.x, x.y * g.y, x.z * g.z, x.w * g.w);
+      }
     }
     ss = warp_sum(ss);
     inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);

@@ -26,6 +26,53 @@ def raw_rows(rep):
     return [(dict(zip(hdr, r)), dict(zip(hdr, units))) for r in rows[2:]]
 
 
+def _record(row, unit, kernel, workload, rep):
+    rec = {"kernel": kernel, "workload": workload, "name": row.get("Kernel Name", "")[:120],
+           "report": os.path.basename(rep)}
+    for k in KEYS:
+        if k in row and row[k] not in ("", None):
+            v = float(row[k].replace(",", ""))
+            u = unit.get(k, "")
+            if u in SCALE:
+                v *= SCALE[u]
+            rec[k] = v
+            rec[k + ".unit"] = "byte" if u in SCALE else u
+    rec["dram_bytes_per_launch"] = rec.get("dram__bytes_read.sum", 0) + rec.get("dram__bytes_write.sum", 0)
+    return rec
+
+
+def _save(keep):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    data = {"kernels": keep,
+            "note": ("one `ncu --set full --clock-control none` capture per kernel/workload (cold-cache, serialised "
+                     "replays); dram_bytes_per_launch = dram__bytes_read.sum + dram__bytes_write.sum")}
+    with open(path, "w") as fh:
+        json.dump(data, fh, indent=1)
+
+
+def _load():
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    return json.load(open(path))["kernels"] if os.path.exists(path) else []
+
+
+def main_named(rep, workload, name_of):
+    """Every kernel of `rep` under its base name (name_of(full name)); the first
+    launch of each name wins (the report holds one layer call)."""
+    keep = _load()
+    done = set()
+    for row, unit in raw_rows(rep):
+        kernel = name_of(row.get("Kernel Name", ""))
+        if kernel in done:
+            continue
+        done.add(kernel)
+        rec = _record(row, unit, kernel, workload, rep)
+        keep = [k for k in keep if not (k["kernel"] == kernel and k["workload"] == workload)]
+        keep.append(rec)
+        print(json.dumps({k: rec[k] for k in ("kernel", "workload", "gpu__time_duration.sum", "dram_bytes_per_launch")
+                          if k in rec}))
+    _save(keep)
+
+
 def main(args):
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     data = json.load(open(path)) if os.path.exists(path) else {"kernels": []}
