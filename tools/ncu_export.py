@@ -47,21 +47,32 @@ def main(rep, workload, out):
         for nm in seen:
             src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{re.escape(nm)}"],
                                  capture_output=True, text=True).stdout
-            lines = list(csv.reader(io.StringIO(src)))
-            if len(lines) < 3:
+            sections, cur, hdr = [], None, None
+            for r in csv.reader(io.StringIO(src)):
+                if not r:
+                    continue
+                if r[0] == "Kernel Name":
+                    cur = []
+                    sections.append(cur)
+                    hdr = None
+                elif r[0] == "Address":
+                    hdr = r
+                elif hdr is not None and cur is not None:
+                    cur.append(dict(zip(hdr, r)))
+            if not sections or not sections[0]:
                 continue
-            hdr = lines[1] if lines[0] and lines[0][0] == "Kernel Name" else lines[0]
-            data = lines[2:] if hdr is lines[1] else lines[1:]
-            try:
-                si = hdr.index("Warp Stall Sampling (All Samples)")
-                sc = hdr.index("Source")
-            except ValueError:
-                continue
-            tot = sum(float(r[si] or 0) for r in data if len(r) > si)
+            data = sections[0]  # first launch of this kernel in the report
+            key = "Warp Stall Sampling (All Samples)"
+
+            def num(r):
+                try:
+                    return float(r.get(key) or 0)
+                except ValueError:
+                    return 0.0
+            tot = sum(num(r) for r in data)
             fh.write(f"== {nm}: {tot:.0f} warp-stall samples; top SASS lines\n")
-            top = sorted((r for r in data if len(r) > si), key=lambda r: -float(r[si] or 0))[:25]
-            for r in top:
-                fh.write(f"{float(r[si] or 0):7.0f}  {r[sc][:120]}\n")
+            for r in sorted(data, key=lambda r: -num(r))[:25]:
+                fh.write(f"{num(r):7.0f}  {r.get('Source', '')[:120]}\n")
             fh.write("\n")
     del args
 
