@@ -575,3 +575,25 @@ def test_tcgen05_pair_matches_single_sm():
     ok = topk_margin_ok(ref.decision.logits, 8, 1e-5) & mask_margin_ok(ref, 1e-5)
     assert_kept(ok)
     assert normwise_rel(_np(o2.float()).astype(np.float64)[ok], ref.out[ok]) <= TOL_BF16
+
+
+@pytest.mark.parametrize("t,path", [(8, "auto"), (64, "auto"), (300, "tc")])
+def test_shared_experts_bf16_q30(t, path):
+    """Shared experts (beam.py:163-164: always-on, weight 1.0, added after the
+    routed ones) on the bf16 expert paths at d = 2048: weight streaming (decode)
+    and the tcgen05 grouped GEMM (T = 300, forced), against the fp64 oracle."""
+    try:
+        B.set_expert_path(path)
+        ob, gb, h64, ref, out, dec, md = _layer_case(2048, 768, 128, 8, t, 900 + t, 1 / np.sqrt(2048), "bf16",
+                                                     shared=2, h_dtype=torch.bfloat16)
+    finally:
+        B.set_expert_path("auto")
+    ok = topk_margin_ok(ref.decision.logits, 8, 1e-5) & mask_margin_ok(ref, 1e-5)
+    assert_kept(ok)
+    assert np.array_equal(_np(dec.topk_indices)[ok], ref.decision.topk_indices[ok])
+    o = _np(out.float()).astype(np.float64)
+    assert normwise_rel(o[ok], ref.out[ok]) <= TOL_BF16
+    y = o - h64
+    assert normwise_rel(y[ok], ref.y[ok]) <= 5 * TOL_BF16
+    # a token with every routed slot masked still gets its shared experts
+    assert np.abs(ref.y).max() > 0
