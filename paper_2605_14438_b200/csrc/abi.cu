@@ -90,7 +90,7 @@ struct LayerWs {
   PlanDev plan;
   float* act;
   float* opair;
-  float* xw;       // [T, d_pad] x * norm_w, fp32 (decode: written by the fused gate)
+  float* xw;       // [T, d_pad] x * norm_w, fp32, then the same rows in bf16 (decode: written by the gate)
 };
 
 // One layout serves every entry (sized for the largest user, beam_layer_forward).
@@ -128,7 +128,7 @@ static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, La
   w.plan.slot_expert = c.take<int32_t>(M);
   w.act = w.tc ? nullptr : c.take<float>(cap * g.f_pad);
   w.opair = c.take<float>(cap * g.d_pad);
-  w.xw = (T <= 64 && L.has_norm) ? c.take<float>((size_t)T * g.d_pad) : nullptr;
+  w.xw = (T <= 64 && L.has_norm) ? c.take<float>((size_t)T * g.d_pad * 3 / 2 + 4) : nullptr;
   if (o) *o = w;
   return c.off + 256;
 }
@@ -396,7 +396,8 @@ static int layer_forward(const beam_layer_t* layer, const beam_route_t* route, c
     prof_mark(4, s);
   } else {
     if (prescaled)
-      BEAM_TRY(launch_gateup_simt(L, g, w.xw, BEAM_F32, T, w.inv, nullptr, w.plan, w.act, s, (long long)T * sp.Keff));
+      BEAM_TRY(launch_gateup_simt(L, g, w.xw, BEAM_F32, T, w.inv, nullptr, w.plan, w.act, s, (long long)T * sp.Keff,
+                                  w.xw + (size_t)T * g.d_pad));
     else
       BEAM_TRY(launch_gateup_simt(L, g, X, h_dtype, T, L.has_norm ? w.inv : nullptr,
                                   L.has_norm ? L.norm_w : nullptr, w.plan, w.act, s));
@@ -505,7 +506,7 @@ static size_t ep_carve(const beam_layer_t& L, int n, int K, int mode, void* ws, 
   size_t off = carve(L, n, K, 1, ws, o, 0, mode == 1 ? 0 : mode == 2 ? 1 : -1);
   off = (off + 255) & ~size_t(255);
   if (xw) *xw = ws ? reinterpret_cast<float*>(static_cast<char*>(ws) + off) : nullptr;
-  return off + (L.has_norm ? (size_t)n * g.d_pad * sizeof(float) : 0) + 256;
+  return off + (L.has_norm ? (size_t)n * g.d_pad * (sizeof(float) + sizeof(__nv_bfloat16)) : 0) + 256;
 }
 
 size_t beam_ep_workspace_bytes(const beam_layer_t* local, int n, int K, int mode) {
@@ -540,7 +541,8 @@ int beam_ep_execute(const beam_layer_t* local, const void* x, int x_dtype, int n
     BEAM_TRY(launch_pack_x(X, x_dtype, inv, L.has_norm ? L.norm_w : nullptr, g, w.plan, w.cap, w.xperm, s));
     BEAM_TRY(launch_experts_tc(L, g, w.xperm, w.plan, w.cap, w.act16, w.opair, s));
   } else if (prescale) {
-    BEAM_TRY(launch_gateup_simt(L, g, xw, BEAM_F32, n, inv, nullptr, w.plan, w.act, s, (long long)n * K));
+    BEAM_TRY(launch_gateup_simt(L, g, xw, BEAM_F32, n, inv, nullptr, w.plan, w.act, s, (long long)n * K,
+                                xw + (size_t)n * g.d_pad));
     BEAM_TRY(launch_down_simt(L, g, n, w.plan, w.act, w.opair, s));
   } else {
     const void* X = nullptr;

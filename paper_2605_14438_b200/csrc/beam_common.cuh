@@ -80,6 +80,13 @@ template <typename T> __device__ __forceinline__ T from_f32(float v);
 template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
 template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
+// (lo, hi) -> one 32-bit word of two bf16 (round to nearest even), lo in the low half
+__device__ __forceinline__ uint32_t bf16x2_pack(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // programmatic dependent launch (PDL): kernels of the layer chain are launched
 // with programmatic stream serialization, so a kernel's launch and prologue

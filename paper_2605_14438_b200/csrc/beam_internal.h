@@ -134,14 +134,16 @@ cudaError_t launch_plan_prepare(const int32_t* counts, const int32_t* offsets,
 // experts_simt.cu
 // slots: planned (token, slot) entries when the caller knows them (T * Keff),
 // -1 = unknown; only prunes the MMA launch, never changes results
+// act: [cap, f_pad] rows in the weight dtype (bf16 or fp32) between the two stages
+// X16 (optional): the same rows as X in bf16 — the tensor-core items' operand
 cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
-                               const float* inv, const float* nw, const PlanDev& p, float* act,
-                               cudaStream_t s, long long slots = -1);
+                               const float* inv, const float* nw, const PlanDev& p, void* act,
+                               cudaStream_t s, long long slots = -1, const void* X16 = nullptr);
 cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const PlanDev& p,
-                             const float* act, float* opair, cudaStream_t s, long long slots = -1);
+                             const void* act, float* opair, cudaStream_t s, long long slots = -1);
 // Decode expert stage on externally routed rows (no norm): gate/up then down.
 inline cudaError_t launch_experts_simt(const beam_layer_t& L, const Dims& g, const void* X,
-                                       int x_dtype, int T, const PlanDev& p, float* act, float* opair,
+                                       int x_dtype, int T, const PlanDev& p, void* act, float* opair,
                                        cudaStream_t s) {
   cudaError_t e = launch_gateup_simt(L, g, X, x_dtype, T, nullptr, nullptr, p, act, s);
   if (e != cudaSuccess) return e;

@@ -176,12 +176,15 @@ __global__ void __launch_bounds__(256) ep_unpack_kernel(const int32_t* __restric
     gw[i] = __int_as_float(meta[r * MW + K + k]);
     if (k == 0) inv[r] = __int_as_float(meta[r * MW + 2 * K]);
   }
-  if (xw != nullptr) {
+  if (xw != nullptr) {  // fp32 rows, then their bf16 copy behind all n rows (tensor-core items)
+    __nv_bfloat16* xw16 = reinterpret_cast<__nv_bfloat16*>(xw + (size_t)n * d_pad);
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)n * d_pad;
          i += (long long)gridDim.x * blockDim.x) {
       const long long r = i / d_pad;
       const int k = (int)(i - r * d_pad);
-      xw[i] = k < d ? to_f32<TX>(x[r * d + k]) * nw[k] : 0.0f;
+      const float v = k < d ? to_f32<TX>(x[r * d + k]) * nw[k] : 0.0f;
+      xw[i] = v;
+      xw16[i] = __float2bfloat16_rn(v);
     }
   }
 }

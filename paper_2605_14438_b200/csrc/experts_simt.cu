@@ -55,7 +55,7 @@ __device__ __forceinline__ void gateup_cta_tile(const TW* __restrict__ W, int ro
                                             const TX* __restrict__ X, const float* __restrict__ inv,
                                             const float* __restrict__ nw, int d, int d_pad, int f_pad,
                                             int feat0, const int32_t* __restrict__ tokp, int pos0,
-                                            int ntok, float* __restrict__ act, float* part,
+                                            int ntok, TW* __restrict__ act, float* part,
                                             float* red) {
   constexpr int EPC = Chunk<TW>::kElems;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -110,7 +110,7 @@ __device__ __forceinline__ void gateup_cta_tile(const TW* __restrict__ W, int ro
       // x_n = x * inv_rms * w: the per-token inv_rms factors out of the dot product
       const float s = inv ? inv[tk[j]] : 1.0f;
       const float gs = red[p * TB + j] * s, u = red[(4 + p) * TB + j] * s;
-      act[(size_t)(pos0 + j) * f_pad + feat0 + p] = activation<ACT>(gs) * u;
+      act[(size_t)(pos0 + j) * f_pad + feat0 + p] = from_f32<TW>(activation<ACT>(gs) * u);
     }
   }
 }
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm) gateup_cta_kernel(const T
                                                              const float* __restrict__ inv,
                                                              const float* __restrict__ nw, int d,
                                                              int d_pad, int f_pad, PlanDev p,
-                                                             float* __restrict__ act) {
+                                                             TW* __restrict__ act) {
   __shared__ float part[kWarps * 32];
   __shared__ float red[32];
   griddep_wait();
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm) gateup_cta_kernel(const T
 // ---------------------------------------------------------------------------
 template <typename TW, int TB>
 __device__ __forceinline__ void down_cta_tile(const TW* __restrict__ W, int row0, int rows_valid,
-                                          const float* __restrict__ act, int f_pad, int d_pad,
+                                          const TW* __restrict__ act, int f_pad, int d_pad,
                                           int pos0, int ntok, const float* __restrict__ wpos,
                                           float* __restrict__ opair, float* part, float* red) {
   constexpr int EPC = Chunk<TW>::kElems;
@@ -167,7 +167,7 @@ __device__ __forceinline__ void down_cta_tile(const TW* __restrict__ W, int row0
   float acc[8 * TB];
 #pragma unroll
   for (int i = 0; i < 8 * TB; ++i) acc[i] = 0.0f;
-  const float* ar[TB];
+  const TW* ar[TB];
 #pragma unroll
   for (int j = 0; j < TB; ++j) ar[j] = act + (size_t)(pos0 + (j < ntok ? j : 0)) * f_pad;
 
@@ -179,15 +179,7 @@ __device__ __forceinline__ void down_cta_tile(const TW* __restrict__ W, int row0
       for (int q = 0; q < 8; ++q) wv[q] = ld_stream(wbase + q * f_pad + c * EPC);
       float af[TB][EPC];
 #pragma unroll
-      for (int j = 0; j < TB; ++j)
-#pragma unroll
-        for (int v = 0; v < EPC / 4; ++v) {
-          const float4 x = __ldg(reinterpret_cast<const float4*>(ar[j] + c * EPC) + v);
-          af[j][4 * v + 0] = x.x;
-          af[j][4 * v + 1] = x.y;
-          af[j][4 * v + 2] = x.z;
-          af[j][4 * v + 3] = x.w;
-        }
+      for (int j = 0; j < TB; ++j) load_x<TW, EPC>(ar[j] + c * EPC, af[j]);  // act rows in the weights' dtype
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float wf[EPC];
@@ -218,7 +210,7 @@ __device__ __forceinline__ void down_cta_tile(const TW* __restrict__ W, int row0
 
 template <typename TW>
 __global__ void __launch_bounds__(kThreads, kCtaPerSm) down_cta_kernel(const TW* __restrict__ Wd,
-                                                           const float* __restrict__ act, int d_pad,
+                                                           const TW* __restrict__ act, int d_pad,
                                                            int f_pad, PlanDev p,
                                                            float* __restrict__ opair) {
   __shared__ float part[kWarps * 32];
@@ -257,7 +249,7 @@ __device__ __forceinline__ void gateup_warp_tile(const TW* __restrict__ W, int r
                                                  const TX* __restrict__ X, const float* __restrict__ inv,
                                                  const float* __restrict__ nw, int d, int d_pad, int f_pad,
                                                  int feat0, const int32_t* __restrict__ tokp, int pos0,
-                                                 int ntok, float* __restrict__ act, float* red, int lane) {
+                                                 int ntok, TW* __restrict__ act, float* red, int lane) {
   constexpr int EPC = Chunk<TW>::kElems;
   const int nch = d_pad / EPC;
   int tk[TB];
@@ -302,7 +294,7 @@ __device__ __forceinline__ void gateup_warp_tile(const TW* __restrict__ W, int r
     if (j < ntok) {
       const float s = inv ? inv[tk[j]] : 1.0f;
       const float gs = red[p * TB + j] * s, u = red[(4 + p) * TB + j] * s;
-      act[(size_t)(pos0 + j) * f_pad + feat0 + p] = activation<ACT>(gs) * u;
+      act[(size_t)(pos0 + j) * f_pad + feat0 + p] = from_f32<TW>(activation<ACT>(gs) * u);
     }
   }
   __syncwarp();
@@ -312,7 +304,7 @@ template <typename TW, typename TX, int ACT>
 __device__ __forceinline__ void gateup_warp_items(const TW* __restrict__ Wgu, const TX* __restrict__ X,
                                                   const float* __restrict__ inv, const float* __restrict__ nw,
                                                   int d, int d_pad, int f_pad, PlanDev p,
-                                                  float* __restrict__ act, float (*red_s)[32]) {
+                                                  TW* __restrict__ act, float (*red_s)[32]) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * kWarps + wib, nwarps = gridDim.x * kWarps;
   const int groups = f_pad / 4;
@@ -349,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_warp_kernel(const TW* __re
                                                                   const float* __restrict__ inv,
                                                                   const float* __restrict__ nw, int d,
                                                                   int d_pad, int f_pad, PlanDev p,
-                                                                  float* __restrict__ act) {
+                                                                  TW* __restrict__ act) {
   __shared__ float red_s[kWarps][32];
   griddep_wait();
   gateup_warp_items<TW, TX, ACT>(Wgu, X, inv, nw, d, d_pad, f_pad, p, act, red_s);
@@ -357,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_warp_kernel(const TW* __re
 
 template <typename TW, int TB>
 __device__ __forceinline__ void down_warp_tile(const TW* __restrict__ W, int row0,
-                                               const float* __restrict__ act, int f_pad, int d_pad,
+                                               const TW* __restrict__ act, int f_pad, int d_pad,
                                                int pos0, int ntok, const float* __restrict__ wpos,
                                                float* __restrict__ opair, float* red, int lane) {
   constexpr int EPC = Chunk<TW>::kElems;
@@ -365,7 +357,7 @@ __device__ __forceinline__ void down_warp_tile(const TW* __restrict__ W, int row
   float acc[8 * TB];
 #pragma unroll
   for (int i = 0; i < 8 * TB; ++i) acc[i] = 0.0f;
-  const float* ar[TB];
+  const TW* ar[TB];
 #pragma unroll
   for (int j = 0; j < TB; ++j) ar[j] = act + (size_t)(pos0 + (j < ntok ? j : 0)) * f_pad;
   const TW* wbase = W + (size_t)row0 * f_pad;
@@ -375,15 +367,7 @@ __device__ __forceinline__ void down_warp_tile(const TW* __restrict__ W, int row
     for (int q = 0; q < 8; ++q) wv[q] = ld_stream(wbase + q * f_pad + c * EPC);
     float af[TB][EPC];
 #pragma unroll
-    for (int j = 0; j < TB; ++j)
-#pragma unroll
-      for (int v = 0; v < EPC / 4; ++v) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(ar[j] + c * EPC) + v);
-        af[j][4 * v + 0] = x.x;
-        af[j][4 * v + 1] = x.y;
-        af[j][4 * v + 2] = x.z;
-        af[j][4 * v + 3] = x.w;
-      }
+    for (int j = 0; j < TB; ++j) load_x<TW, EPC>(ar[j] + c * EPC, af[j]);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       float wf[EPC];
@@ -403,7 +387,7 @@ __device__ __forceinline__ void down_warp_tile(const TW* __restrict__ W, int row
 }
 
 template <typename TW>
-__device__ __forceinline__ void down_warp_items(const TW* __restrict__ Wd, const float* __restrict__ act, int d_pad,
+__device__ __forceinline__ void down_warp_items(const TW* __restrict__ Wd, const TW* __restrict__ act, int d_pad,
                                                 int f_pad, PlanDev p, float* __restrict__ opair,
                                                 float (*red_s)[32]) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -436,7 +420,7 @@ __device__ __forceinline__ void down_warp_items(const TW* __restrict__ Wd, const
 
 template <typename TW>
 __global__ void __launch_bounds__(kThreads, 2) down_warp_kernel(const TW* __restrict__ Wd,
-                                                                const float* __restrict__ act, int d_pad,
+                                                                const TW* __restrict__ act, int d_pad,
                                                                 int f_pad, PlanDev p,
                                                                 float* __restrict__ opair) {
   __shared__ float red_s[kWarps][32];
@@ -547,7 +531,7 @@ __device__ __forceinline__ void mma_rows(const __nv_bfloat16* __restrict__ w0p, 
 template <typename TX, int ACT>
 __device__ __forceinline__ void gateup_mma_items(const __nv_bfloat16* __restrict__ Wgu, const TX* __restrict__ X,
                                                  const float* __restrict__ inv, int d_pad, int f_pad,
-                                                 PlanDev p, float* __restrict__ act) {
+                                                 PlanDev p, __nv_bfloat16* __restrict__ act) {
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5), nwarps = gridDim.x * kWarps;
   const int groups = f_pad / 8;
@@ -572,14 +556,14 @@ __device__ __forceinline__ void gateup_mma_items(const __nv_bfloat16* __restrict
         const int n = 2 * q + j;
         if (n < nt) {
           const float s = inv ? inv[tokp[n]] : 1.0f;
-          act[(size_t)(off + t0 + n) * f_pad + feat0 + g] = activation<ACT>(c[j] * s) * (c[2 + j] * s);
+          act[(size_t)(off + t0 + n) * f_pad + feat0 + g] = __float2bfloat16_rn(activation<ACT>(c[j] * s) * (c[2 + j] * s));
         }
       }
     }
   }
 }
 
-__device__ __forceinline__ void down_mma_items(const __nv_bfloat16* __restrict__ Wd, const float* __restrict__ act,
+__device__ __forceinline__ void down_mma_items(const __nv_bfloat16* __restrict__ Wd, const __nv_bfloat16* __restrict__ act,
                                                int d_pad, int f_pad, PlanDev p, float* __restrict__ opair) {
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5), nwarps = gridDim.x * kWarps;
@@ -598,7 +582,8 @@ __device__ __forceinline__ void down_mma_items(const __nv_bfloat16* __restrict__
       const int nt = min(8, cnt - t0);
       const int pos0 = off + t0;
       float c[4] = {0.f, 0.f, 0.f, 0.f};
-      mma_rows<float>(w0p, w1p, act + (size_t)(pos0 + (g < nt ? g : 0)) * f_pad, f_pad, q, c);
+      // bf16 act rows: one k16 MMA pair per step (no hi / lo split)
+      mma_rows<__nv_bfloat16>(w0p, w1p, act + (size_t)(pos0 + (g < nt ? g : 0)) * f_pad, f_pad, q, c);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int n = 2 * q + j;
@@ -634,7 +619,7 @@ template <typename TX, int ACT>
 __global__ void __launch_bounds__(kThreads, 2) gateup_mma_kernel(const __nv_bfloat16* __restrict__ Wgu,
                                                                  const TX* __restrict__ X,
                                                                  const float* __restrict__ inv, int d_pad,
-                                                                 int f_pad, PlanDev p, float* __restrict__ act) {
+                                                                 int f_pad, PlanDev p, __nv_bfloat16* __restrict__ act) {
   griddep_wait();
   if (use_mma_items(p, f_pad / 8, kMmaTokGateUp)) gateup_mma_items<TX, ACT>(Wgu, X, inv, d_pad, f_pad, p, act);
 }
@@ -644,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_ffma_kernel(const __nv_bfl
                                                                   const float* __restrict__ inv,
                                                                   const float* __restrict__ nw, int d,
                                                                   int d_pad, int f_pad, PlanDev p,
-                                                                  float* __restrict__ act) {
+                                                                  __nv_bfloat16* __restrict__ act) {
   // nw is always null here; a runtime argument keeps the register allocation of
   // gateup_warp_kernel (a literal null makes ptxas spill)
   __shared__ float red_s[kWarps][32];
@@ -654,13 +639,13 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_ffma_kernel(const __nv_bfl
 }
 
 __global__ void __launch_bounds__(kThreads, 2) down_mma_kernel(const __nv_bfloat16* __restrict__ Wd,
-                                                               const float* __restrict__ act, int d_pad,
+                                                               const __nv_bfloat16* __restrict__ act, int d_pad,
                                                                int f_pad, PlanDev p, float* __restrict__ opair) {
   griddep_wait();
   if (use_mma_items(p, (d_pad + 15) / 16, kMmaTokDown)) down_mma_items(Wd, act, d_pad, f_pad, p, opair);
 }
 __global__ void __launch_bounds__(kThreads, 2) down_ffma_kernel(const __nv_bfloat16* __restrict__ Wd,
-                                                                const float* __restrict__ act, int d_pad,
+                                                                const __nv_bfloat16* __restrict__ act, int d_pad,
                                                                 int f_pad, PlanDev p, float* __restrict__ opair) {
   __shared__ float red_s[kWarps][32];
   griddep_wait();
@@ -690,24 +675,32 @@ static bool mma_enabled() {
 // ---------------------------------------------------------------------------
 template <typename TW, typename TX>
 static void gateup_dispatch(const beam_layer_t& L, const Dims& g, const void* X, const float* inv,
-                            const float* nw, const PlanDev& p, float* act, int grid, bool cta,
-                            long long slots, cudaStream_t s) {
+                            const float* nw, const PlanDev& p, void* act_v, int grid, bool cta,
+                            long long slots, cudaStream_t s, const void* X16) {
+  TW* act = static_cast<TW*>(act_v);  // act rows in the weights' dtype
   if (cta) {
     if (L.activation == BEAM_ACT_SILU)
       launch_pdl(gateup_cta_kernel<TW, TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, (const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
     else
       launch_pdl(gateup_cta_kernel<TW, TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, (const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
   } else if (std::is_same<TW, __nv_bfloat16>::value && nw == nullptr && mma_enabled()) {
-    const __nv_bfloat16* W = (const __nv_bfloat16*)L.w_gu;
-    const bool mma = mma_possible(slots, g.f_pad / 8, kMmaTokGateUp, grid);
-    if (L.activation == BEAM_ACT_SILU) {
-      if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act);
-      launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
-    } else {
-      if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act);
-      launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+    if constexpr (std::is_same<TW, __nv_bfloat16>::value) {  // bf16 act rows
+      const __nv_bfloat16* W = (const __nv_bfloat16*)L.w_gu;
+      const bool mma = mma_possible(slots, g.f_pad / 8, kMmaTokGateUp, grid);
+      // tensor-core items read the bf16 copy of the rows when there is one
+      // (one MMA pair per step instead of the fp32 hi + lo pairs)
+      const bool b16 = X16 != nullptr;
+      if (L.activation == BEAM_ACT_SILU) {
+        if (mma && b16) launch_pdl(gateup_mma_kernel<__nv_bfloat16, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const __nv_bfloat16*)X16, inv, g.d_pad, g.f_pad, p, act);
+        else if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act);
+        launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+      } else {
+        if (mma && b16) launch_pdl(gateup_mma_kernel<__nv_bfloat16, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const __nv_bfloat16*)X16, inv, g.d_pad, g.f_pad, p, act);
+        else if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act);
+        launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+      }
+      if (mma) count_launches(1);
     }
-    if (mma) count_launches(1);
   } else {
     if (L.activation == BEAM_ACT_SILU)
       launch_pdl(gateup_warp_kernel<TW, TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, (const TW*)L.w_gu, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
@@ -722,38 +715,38 @@ static void gateup_dispatch(const beam_layer_t& L, const Dims& g, const void* X,
 static bool small_batch(int T) { return T <= 2; }
 
 cudaError_t launch_gateup_simt(const beam_layer_t& L, const Dims& g, const void* X, int x_dtype, int T,
-                               const float* inv, const float* nw, const PlanDev& p, float* act,
-                               cudaStream_t s, long long slots) {
+                               const float* inv, const float* nw, const PlanDev& p, void* act,
+                               cudaStream_t s, long long slots, const void* X16) {
   const bool xb = x_dtype == BEAM_BF16;
   const bool cta = small_batch(T);
   const int grid = num_sms() * (cta ? kCtaPerSm : 2);
   if (L.wdtype == BEAM_BF16) {
-    if (xb) gateup_dispatch<__nv_bfloat16, __nv_bfloat16>(L, g, X, inv, nw, p, act, grid, cta, slots, s);
-    else gateup_dispatch<__nv_bfloat16, float>(L, g, X, inv, nw, p, act, grid, cta, slots, s);
+    if (xb) gateup_dispatch<__nv_bfloat16, __nv_bfloat16>(L, g, X, inv, nw, p, act, grid, cta, slots, s, X16);
+    else gateup_dispatch<__nv_bfloat16, float>(L, g, X, inv, nw, p, act, grid, cta, slots, s, X16);
   } else {
-    if (xb) gateup_dispatch<float, __nv_bfloat16>(L, g, X, inv, nw, p, act, grid, cta, slots, s);
-    else gateup_dispatch<float, float>(L, g, X, inv, nw, p, act, grid, cta, slots, s);
+    if (xb) gateup_dispatch<float, __nv_bfloat16>(L, g, X, inv, nw, p, act, grid, cta, slots, s, nullptr);
+    else gateup_dispatch<float, float>(L, g, X, inv, nw, p, act, grid, cta, slots, s, nullptr);
   }
   count_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const PlanDev& p,
-                             const float* act, float* opair, cudaStream_t s, long long slots) {
+                             const void* act, float* opair, cudaStream_t s, long long slots) {
   const bool cta = small_batch(T);
   const int grid = num_sms() * (cta ? kCtaPerSm : 2);
   if (L.wdtype == BEAM_BF16) {
-    if (cta) launch_pdl(down_cta_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+    if (cta) launch_pdl(down_cta_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair);
     else if (mma_enabled()) {
       const bool mma = mma_possible(slots, (g.d_pad + 15) / 16, kMmaTokDown, grid);
-      if (mma) launch_pdl(down_mma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
-      launch_pdl(down_ffma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+      if (mma) launch_pdl(down_mma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair);
+      launch_pdl(down_ffma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair);
       if (mma) count_launches(1);
     }
-    else launch_pdl(down_warp_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+    else launch_pdl(down_warp_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair);
   } else {
-    if (cta) launch_pdl(down_cta_kernel<float>, grid, kThreads, 0, s, (const float*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
-    else launch_pdl(down_warp_kernel<float>, grid, kThreads, 0, s, (const float*)L.w_down, act, g.d_pad, g.f_pad, p, opair);
+    if (cta) launch_pdl(down_cta_kernel<float>, grid, kThreads, 0, s, (const float*)L.w_down, (const float*)act, g.d_pad, g.f_pad, p, opair);
+    else launch_pdl(down_warp_kernel<float>, grid, kThreads, 0, s, (const float*)L.w_down, (const float*)act, g.d_pad, g.f_pad, p, opair);
   }
   count_launches(1);
   return cudaGetLastError();

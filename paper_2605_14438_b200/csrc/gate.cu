@@ -237,13 +237,18 @@ __device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const
     if (xw != nullptr) {
       // the norm-weighted token rows x * w (fp32, exactly the product the decode
       // gate/up kernels formed per chunk) for the expert stage: its inner loop
-      // then loads one row per token and does no per-chunk norm multiply
+      // then loads one row per token and does no per-chunk norm multiply; a bf16
+      // copy right behind them ([T, d_pad] after the fp32 rows) feeds the
+      // tensor-core items as one MMA operand
+      __nv_bfloat16* xw16 = reinterpret_cast<__nv_bfloat16*>(xw + (size_t)T * d_pad);
       for (int v = threadIdx.x; v < nt * (kn >> 2); v += 256) {
         const int t = v / (kn >> 2), k4 = v % (kn >> 2);
         const float4 x = *reinterpret_cast<const float4*>(xs + t * kr + 4 * k4);
         const float4 g = ld_norm4(nw, ks + 4 * k4, d);
-        *reinterpret_cast<float4*>(xw + (size_t)(t0 + t) * d_pad + ks + 4 * k4) =
-            make_float4(x.x * g.x, x.y * g.y, x.z * g.z, x.w * g.w);
+        const float4 y = make_float4(x.x * g.x, x.y * g.y, x.z * g.z, x.w * g.w);
+        const size_t o = (size_t)(t0 + t) * d_pad + ks + 4 * k4;
+        *reinterpret_cast<float4*>(xw + o) = y;
+        *reinterpret_cast<uint2*>(xw16 + o) = make_uint2(bf16x2_pack(y.x, y.y), bf16x2_pack(y.z, y.w));
       }
     }
   }

@@ -262,9 +262,12 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
       ss = fmaf(x.y, x.y, ss);
       ss = fmaf(x.z, x.z, ss);
       ss = fmaf(x.w, x.w, ss);
-      if (xw != nullptr) {
+      if (xw != nullptr) {  // fp32 rows, then their bf16 copy behind all T rows
         const float4 g = ld_norm4(a.nw, k, a.d);
-        *reinterpret_cast<float4*>(xw + k) = make_float4(x.x * g.x, x.y * g.y, x.z * g.z, x.w * g.w);
+        const float4 y = make_float4(x.x * g.x, x.y * g.y, x.z * g.z, x.w * g.w);
+        *reinterpret_cast<float4*>(xw + k) = y;
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.xw_out + (size_t)T * a.d_pad) +
+                                  (size_t)t * a.d_pad + k) = make_uint2(bf16x2_pack(y.x, y.y), bf16x2_pack(y.z, y.w));
       }
     }
     ss = warp_sum(ss);

@@ -10,9 +10,11 @@
   every exchange is a CPU collective);
 * NCCL at world size 1 (the collectives as captured by bench.py --gpus N).
 
-Tolerances: with fp32 tokens the fixed-capacity EP step computes the single-GPU
-layer's arithmetic (same prescaled rows, weight-streaming kernels) up to the
-order of the per-rank partial sums -> y within 1e-4; with bf16 tokens `out` is rounded to bf16, so
+Tolerances: with fp32 tokens and one shard the fixed-capacity EP step computes
+the single-GPU layer's arithmetic (same prescaled rows, same plan, same item
+kinds) up to the inv_rms summation order -> y within 1e-4; with several shards
+each rank's plan picks its own item kinds (fp32 FFMA or bf16 tensor-core items),
+so the north-star 1e-2; with bf16 tokens `out` is rounded to bf16, so
 out is compared at the north-star 1e-2 (normwise) and y = out - h up to one bf16
 ulp of |out| plus 1e-2 of max|y|."""
 
@@ -132,7 +134,10 @@ def test_virtual_ep_matches_single_gpu(world, ts, fixed, h_dtype):
             assert o.shape == h.shape
             continue
         ref, _, _ = B.beam_block_forward(h, gb, training=False)
-        _check(o, ref, h, tight=fixed)
+        # one shard sees the single-GPU plan itself (same item kinds, same
+        # arithmetic up to inv_rms summation order); with several shards the
+        # per-rank plans pick FFMA or bf16 tensor-core items on their own
+        _check(o, ref, h, tight=fixed and world == 1)
 
 
 def _worker(rank, world, port, ts, q):
