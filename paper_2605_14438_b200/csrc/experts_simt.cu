@@ -607,9 +607,17 @@ __device__ __forceinline__ bool use_mma_items(const PlanDev& p, int items_per_ex
   const int e_act = p.meta[0];
   return p.meta[2] >= tok_per_expert * e_act && (long long)e_act * items_per_expert >= 3LL * gridDim.x * kWarps;
 }
-// tokens per active expert from which the MMA items win: gate/up 3 (at 2.4 they
-// lose 4 %: T=64 s=0.5 gate/up 134 vs 129 us), down 2 (72 -> 68 us there)
-constexpr int kMmaTokGateUp = 3, kMmaTokDown = 2;
+// tokens per active expert from which the MMA items win.  With bf16 operands on
+// both sides (one MMA pair per 32-k step) gate/up items win from 2 tokens per
+// expert (profiles/r02/mma_tok_ab.txt, Q30: T=32 s=0 241.2 -> 221.4 us, T=64
+// s=0.5 221.6 -> 215.2 us; 1 loses at T=16); down items from 2.
+constexpr int kMmaTokGateUp = 2, kMmaTokDown = 2;
+// (BEAM_MMA_TOK_GU / BEAM_MMA_TOK_DN override the two thresholds: tuning runs)
+static int mma_tok(int which) {
+  static const int v[2] = {[] { const char* e = getenv("BEAM_MMA_TOK_GU"); return e ? atoi(e) : kMmaTokGateUp; }(),
+                           [] { const char* e = getenv("BEAM_MMA_TOK_DN"); return e ? atoi(e) : kMmaTokDown; }()};
+  return v[which];
+}
 
 // Two launches per stage, each leaving at once when the plan picks the other
 // (one kernel holding both bodies spills, or with 2-token FFMA passes runs the
@@ -619,9 +627,10 @@ template <typename TX, int ACT>
 __global__ void __launch_bounds__(kThreads, 2) gateup_mma_kernel(const __nv_bfloat16* __restrict__ Wgu,
                                                                  const TX* __restrict__ X,
                                                                  const float* __restrict__ inv, int d_pad,
-                                                                 int f_pad, PlanDev p, __nv_bfloat16* __restrict__ act) {
+                                                                 int f_pad, PlanDev p, __nv_bfloat16* __restrict__ act,
+                                                                 int tok) {
   griddep_wait();
-  if (use_mma_items(p, f_pad / 8, kMmaTokGateUp)) gateup_mma_items<TX, ACT>(Wgu, X, inv, d_pad, f_pad, p, act);
+  if (use_mma_items(p, f_pad / 8, tok)) gateup_mma_items<TX, ACT>(Wgu, X, inv, d_pad, f_pad, p, act);
 }
 template <typename TX, int ACT>
 __global__ void __launch_bounds__(kThreads, 2) gateup_ffma_kernel(const __nv_bfloat16* __restrict__ Wgu,
@@ -629,27 +638,27 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_ffma_kernel(const __nv_bfl
                                                                   const float* __restrict__ inv,
                                                                   const float* __restrict__ nw, int d,
                                                                   int d_pad, int f_pad, PlanDev p,
-                                                                  __nv_bfloat16* __restrict__ act) {
+                                                                  __nv_bfloat16* __restrict__ act, int tok) {
   // nw is always null here; a runtime argument keeps the register allocation of
   // gateup_warp_kernel (a literal null makes ptxas spill)
   __shared__ float red_s[kWarps][32];
   griddep_wait();
-  if (!use_mma_items(p, f_pad / 8, kMmaTokGateUp))
+  if (!use_mma_items(p, f_pad / 8, tok))
     gateup_warp_items<__nv_bfloat16, TX, ACT>(Wgu, X, inv, nw, d, d_pad, f_pad, p, act, red_s);
 }
 
 __global__ void __launch_bounds__(kThreads, 2) down_mma_kernel(const __nv_bfloat16* __restrict__ Wd,
                                                                const __nv_bfloat16* __restrict__ act, int d_pad,
-                                                               int f_pad, PlanDev p, float* __restrict__ opair) {
+                                                               int f_pad, PlanDev p, float* __restrict__ opair, int tok) {
   griddep_wait();
-  if (use_mma_items(p, (d_pad + 15) / 16, kMmaTokDown)) down_mma_items(Wd, act, d_pad, f_pad, p, opair);
+  if (use_mma_items(p, (d_pad + 15) / 16, tok)) down_mma_items(Wd, act, d_pad, f_pad, p, opair);
 }
 __global__ void __launch_bounds__(kThreads, 2) down_ffma_kernel(const __nv_bfloat16* __restrict__ Wd,
                                                                 const __nv_bfloat16* __restrict__ act, int d_pad,
-                                                                int f_pad, PlanDev p, float* __restrict__ opair) {
+                                                                int f_pad, PlanDev p, float* __restrict__ opair, int tok) {
   __shared__ float red_s[kWarps][32];
   griddep_wait();
-  if (!use_mma_items(p, (d_pad + 15) / 16, kMmaTokDown)) down_warp_items<__nv_bfloat16>(Wd, act, d_pad, f_pad, p, opair, red_s);
+  if (!use_mma_items(p, (d_pad + 15) / 16, tok)) down_warp_items<__nv_bfloat16>(Wd, act, d_pad, f_pad, p, opair, red_s);
 }
 
 // Host side of use_mma_items: E_act * items >= 3 * warps needs E_act >= e_min,
@@ -686,18 +695,19 @@ static void gateup_dispatch(const beam_layer_t& L, const Dims& g, const void* X,
   } else if (std::is_same<TW, __nv_bfloat16>::value && nw == nullptr && mma_enabled()) {
     if constexpr (std::is_same<TW, __nv_bfloat16>::value) {  // bf16 act rows
       const __nv_bfloat16* W = (const __nv_bfloat16*)L.w_gu;
-      const bool mma = mma_possible(slots, g.f_pad / 8, kMmaTokGateUp, grid);
+      const int tok = mma_tok(0);
+      const bool mma = mma_possible(slots, g.f_pad / 8, tok, grid);
       // tensor-core items read the bf16 copy of the rows when there is one
       // (one MMA pair per step instead of the fp32 hi + lo pairs)
       const bool b16 = X16 != nullptr;
       if (L.activation == BEAM_ACT_SILU) {
-        if (mma && b16) launch_pdl(gateup_mma_kernel<__nv_bfloat16, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const __nv_bfloat16*)X16, inv, g.d_pad, g.f_pad, p, act);
-        else if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act);
-        launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+        if (mma && b16) launch_pdl(gateup_mma_kernel<__nv_bfloat16, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const __nv_bfloat16*)X16, inv, g.d_pad, g.f_pad, p, act, tok);
+        else if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act, tok);
+        launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act, tok);
       } else {
-        if (mma && b16) launch_pdl(gateup_mma_kernel<__nv_bfloat16, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const __nv_bfloat16*)X16, inv, g.d_pad, g.f_pad, p, act);
-        else if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act);
-        launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act);
+        if (mma && b16) launch_pdl(gateup_mma_kernel<__nv_bfloat16, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const __nv_bfloat16*)X16, inv, g.d_pad, g.f_pad, p, act, tok);
+        else if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act, tok);
+        launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act, tok);
       }
       if (mma) count_launches(1);
     }
@@ -738,9 +748,10 @@ cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const 
   if (L.wdtype == BEAM_BF16) {
     if (cta) launch_pdl(down_cta_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair);
     else if (mma_enabled()) {
-      const bool mma = mma_possible(slots, (g.d_pad + 15) / 16, kMmaTokDown, grid);
-      if (mma) launch_pdl(down_mma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair);
-      launch_pdl(down_ffma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair);
+      const int tok = mma_tok(1);
+      const bool mma = mma_possible(slots, (g.d_pad + 15) / 16, tok, grid);
+      if (mma) launch_pdl(down_mma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair, tok);
+      launch_pdl(down_ffma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair, tok);
       if (mma) count_launches(1);
     }
     else launch_pdl(down_warp_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair);
