@@ -295,6 +295,13 @@ int beam_ep_combine(const float* y_back, const int32_t* send_pos, int world, int
  *  token 0: partials summed, top-K selected, softmax done, outputs stored}. */
 int beam_trace_gate(unsigned long long* dev_buf);
 const char* beam_last_cuda_error(void);
+/* Device-checked build (libbeam_b200_checked.so, -DBEAM_DEVICE_CHECKS): index
+ * bounds the kernels rely on (plan positions < capacity, token indices < T,
+ * expert ids < E, combine slot positions, tensor-core tiles inside the packed
+ * rows) are asserted on the device; violations OR a bit into *dev_flag (a
+ * zeroed device word; NULL = off).  The regular library returns
+ * BEAM_ERR_UNSUPPORTED. */
+int beam_debug_checks(unsigned* dev_flag);
 /* sizeof the ABI structs (0 beam_layer_t, 1 beam_outputs_t, 2 beam_route_t): lets
  * FFI bindings check their struct mirrors against the compiled library. */
 size_t beam_abi_sizeof(int which);

@@ -12,7 +12,9 @@ import os
 from .tensor import ContractError, ShapeError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libbeam_b200.so")
+# BEAM_LIB=checked loads the device-checked build (bounds assertions, tests only)
+LIB_PATH = os.path.join(_PKG, "_lib", "libbeam_b200_checked.so" if os.environ.get("BEAM_LIB") == "checked"
+                        else "libbeam_b200.so")
 
 BEAM_OK = 0
 BEAM_ERR_ARG = -1
@@ -52,6 +54,7 @@ EXPORTS = (
     "beam_host_mapped",
     "beam_router_split",
     "beam_abi_sizeof",
+    "beam_debug_checks",
     "beam_ep_tiles",
     "beam_ep_count",
     "beam_ep_pack",
@@ -158,6 +161,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "beam_host_mapped": (I, [P]),
         "beam_router_split": (I, [P, P, I, I, I, P, P]),
         "beam_abi_sizeof": (S, [I]),
+        "beam_debug_checks": (I, [P]),
         "beam_ep_tiles": (I, [I]),
         "beam_ep_count": (I, [P, I, I, I, I, P, P]),
         "beam_ep_pack": (I, [P, I, I, I, P, P, I, I, I, I, P, I, P, P, P, P, P]),

@@ -64,6 +64,9 @@ struct Carver {
   }
 };
 
+// Checked build: the device word violations are ORed into (beam_debug_checks).
+static unsigned* g_check_flag = nullptr;
+
 // Expert path choice: 0 = auto, 1 = weight-streaming SIMT, 2 = tcgen05 grouped GEMM.
 static std::atomic<int> g_expert_path{0};
 
@@ -126,6 +129,9 @@ static size_t carve(const beam_layer_t& L, int T, int Kids, int bs, void* ws, La
   w.plan.w = c.take<float>(cap);
   w.plan.slot_pos = c.take<int32_t>(M);
   w.plan.slot_expert = c.take<int32_t>(M);
+  w.plan.cap = (int)cap;
+  w.plan.T = T;
+  w.plan.check = g_check_flag;
   w.act = w.tc ? nullptr : c.take<float>(cap * g.f_pad);
   w.opair = c.take<float>(cap * g.d_pad);
   w.xw = (T <= 64 && L.has_norm) ? c.take<float>((size_t)T * g.d_pad * 3 / 2 + 4) : nullptr;
@@ -772,6 +778,16 @@ int beam_trace_gate(unsigned long long* dev_buf) { return status(beam::set_gate_
 
 const char* beam_last_cuda_error(void) { return g_last_error; }
 
+int beam_debug_checks(unsigned* dev_flag) {
+#ifdef BEAM_DEVICE_CHECKS
+  g_check_flag = dev_flag;
+  return BEAM_OK;
+#else
+  (void)dev_flag;
+  return BEAM_ERR_UNSUPPORTED;  // only libbeam_b200_checked.so carries the checks
+#endif
+}
+
 size_t beam_abi_sizeof(int which) {
   switch (which) {
     case 0: return sizeof(beam_layer_t);
@@ -793,7 +809,11 @@ int beam_host_mapped(const void* p) {
 #define BEAM_STR2(x) #x
 #define BEAM_STR(x) BEAM_STR2(x)
 const char* beam_build_info(void) {
+#ifdef BEAM_DEVICE_CHECKS
+  return "beam_b200 sm_100a nvcc " BEAM_STR(__CUDACC_VER_MAJOR__) "." BEAM_STR(__CUDACC_VER_MINOR__) " device-checked";
+#else
   return "beam_b200 sm_100a nvcc " BEAM_STR(__CUDACC_VER_MAJOR__) "." BEAM_STR(__CUDACC_VER_MINOR__);
+#endif
 }
 
 }  // extern "C"

@@ -88,6 +88,31 @@ __device__ __forceinline__ uint32_t bf16x2_pack(float lo, float hi) {
 }
 
 // ---------------------------------------------------------------------------
+// device-checked build (-DBEAM_DEVICE_CHECKS, libbeam_b200_checked.so): index
+// bounds the kernels rely on are asserted; a violation ORs `code` into the
+// plan's check word (read back by beam_debug_checks) instead of trapping.  The
+// substitute for compute-sanitizer memcheck, which this GPU pool does not run.
+// ---------------------------------------------------------------------------
+enum : unsigned {
+  kChkPlanPos = 1u,      // a plan position outside [0, cap)
+  kChkExpert = 2u,       // an expert id outside [0, E)
+  kChkToken = 4u,        // a token index outside [0, T)
+  kChkSlotPos = 8u,      // a combine slot position outside [0, cap)
+  kChkTile = 16u,        // a tensor-core tile reaching past the packed rows
+  kChkEpRow = 32u,       // an expert-parallel send row outside its buffer
+};
+#ifdef BEAM_DEVICE_CHECKS
+#define BEAM_DCHECK(plan, cond, code)                                    \
+  do {                                                                   \
+    if ((plan).check != nullptr && !(cond)) atomicOr((plan).check, (code)); \
+  } while (0)
+#else
+#define BEAM_DCHECK(plan, cond, code) \
+  do {                                \
+  } while (0)
+#endif
+
+// ---------------------------------------------------------------------------
 // programmatic dependent launch (PDL): kernels of the layer chain are launched
 // with programmatic stream serialization, so a kernel's launch and prologue
 // overlap its predecessor's tail; griddep_wait() blocks until the predecessor

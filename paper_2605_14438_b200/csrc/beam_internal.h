@@ -42,6 +42,10 @@ struct PlanDev {
   float* w;              // [cap] routing weight of each planned position
   int32_t* slot_pos;     // [T*Keff] position of (t,k) in the plan, -1 if dropped
   int32_t* slot_expert;  // [T*Keff] expert of (t,k), -1 if dropped
+  // device-checked build (BEAM_DEVICE_CHECKS): allocation bounds of the plan and
+  // the flag word violations are ORed into (beam_debug_checks); 0 / null = off
+  int cap = 0, T = 0;
+  unsigned* check = nullptr;
 };
 
 // Arguments of the per-token top-K / softmax / mask step (route_device.cuh).

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(32 * kCombineWarps, 3) combine_kernel(const in
                                                                      const int32_t* __restrict__ slot_pos,
                                                                      const TP* __restrict__ opair, int T, int Keff,
                                                                      int d, int d_pad, const TH* __restrict__ h,
-                                                                     TO* __restrict__ out, bool vec) {
+                                                                     TO* __restrict__ out, bool vec, PlanDev chk) {
   griddep_wait();
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * kCombineWarps + (threadIdx.x >> 5);
@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(32 * kCombineWarps, 3) combine_kernel(const in
   // slots with a smaller position (no second, dependent load of the slot's expert)
   int pos = -1;
   if (lane < Keff) pos = slot_pos[(size_t)t * Keff + lane];
+  BEAM_DCHECK(chk, chk.cap == 0 || pos < chk.cap, kChkSlotPos);
   int rank = 0, nv = 0;
 #pragma unroll 4
   for (int j = 0; j < min(Keff, 32); ++j) {
@@ -161,12 +162,12 @@ static cudaError_t combine_dispatch(const PlanDev& p, const TP* opair, int T, in
   const dim3 grid(tiles, gy);
   const int thr = 32 * kCombineWarps;
   if (out_dtype == BEAM_F32 && h_dtype == BEAM_F32)
-    return launch_pdl(combine_kernel<float, float, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const float*)h, (float*)out, vec);
+    return launch_pdl(combine_kernel<float, float, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const float*)h, (float*)out, vec, p);
   if (out_dtype == BEAM_BF16 && h_dtype == BEAM_BF16)
-    return launch_pdl(combine_kernel<__nv_bfloat16, __nv_bfloat16, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const __nv_bfloat16*)h, (__nv_bfloat16*)out, vec);
+    return launch_pdl(combine_kernel<__nv_bfloat16, __nv_bfloat16, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const __nv_bfloat16*)h, (__nv_bfloat16*)out, vec, p);
   if (out_dtype == BEAM_F32)
-    return launch_pdl(combine_kernel<__nv_bfloat16, float, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const __nv_bfloat16*)h, (float*)out, vec);
-  return launch_pdl(combine_kernel<float, __nv_bfloat16, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const float*)h, (__nv_bfloat16*)out, vec);
+    return launch_pdl(combine_kernel<__nv_bfloat16, float, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const __nv_bfloat16*)h, (float*)out, vec, p);
+  return launch_pdl(combine_kernel<float, __nv_bfloat16, TP>, grid, thr, 0, s, p.slot_expert, p.slot_pos, opair, T, Keff, d, d_pad, (const float*)h, (__nv_bfloat16*)out, vec, p);
 }
 
 cudaError_t launch_combine(const PlanDev& p, const void* opair, int opair_dtype, int T, int Keff, int d, int d_pad,

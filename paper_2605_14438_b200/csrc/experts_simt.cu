@@ -47,6 +47,20 @@ __device__ __forceinline__ void load_x(const TX* __restrict__ p, float* out) {
   }
 }
 
+// Checked build: an item's plan run [off, off + cnt) lies inside the plan and
+// its token indices inside [0, T) (lane 0 of the first item of each expert).
+__device__ __forceinline__ void check_item(const PlanDev& p, int off, int cnt, bool first) {
+#ifdef BEAM_DEVICE_CHECKS
+  if (p.check == nullptr || !first) return;
+  BEAM_DCHECK(p, p.cap == 0 || (off >= 0 && off + cnt <= p.cap), kChkPlanPos);
+  if (p.T > 0)
+    for (int q = 0; q < cnt; ++q) {
+      const int t = p.tok[off + q];
+      BEAM_DCHECK(p, t >= 0 && t < p.T, kChkToken);
+    }
+#endif
+}
+
 // ---------------------------------------------------------------------------
 // gate / up
 // ---------------------------------------------------------------------------
@@ -131,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm) gateup_cta_kernel(const T
     const int a = (int)(item / groups), g = (int)(item % groups);
     const int e = p.active[a];
     const int cnt = p.counts[e], off = p.offsets[e];
+    if (threadIdx.x == 0) check_item(p, off, cnt, g == 0);
     const TW* W = Wgu + (size_t)e * 2 * f_pad * d_pad;
     const int feat0 = g * 4;
     const int row_g = (feat0 >> 4) * 32 + (feat0 & 15);
@@ -222,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm) down_cta_kernel(const TW*
     const int a = (int)(item / groups), g = (int)(item % groups);
     const int e = p.active[a];
     const int cnt = p.counts[e], off = p.offsets[e];
+    if (threadIdx.x == 0) check_item(p, off, cnt, g == 0);
     const TW* W = Wd + (size_t)e * d_pad * f_pad;
     const int row0 = g * 16, rows_valid = min(16, d_pad - row0);
     for (int t0 = 0; t0 < cnt;) {  // T <= 2 (small_batch): at most 2 tokens per expert
@@ -313,6 +329,7 @@ __device__ __forceinline__ void gateup_warp_items(const TW* __restrict__ Wgu, co
     const int a = (int)(item / groups), g = (int)(item % groups);
     const int e = p.active[a];
     const int cnt = p.counts[e], off = p.offsets[e];
+    if (lane == 0) check_item(p, off, cnt, g == 0);
     const TW* W = Wgu + (size_t)e * 2 * f_pad * d_pad;
     const int feat0 = g * 4;
     const int row_g = (feat0 >> 4) * 32 + (feat0 & 15);
@@ -398,6 +415,7 @@ __device__ __forceinline__ void down_warp_items(const TW* __restrict__ Wd, const
     const int a = (int)(item / groups), g = (int)(item % groups);
     const int e = p.active[a];
     const int cnt = p.counts[e], off = p.offsets[e];
+    if (lane == 0) check_item(p, off, cnt, g == 0);
     const TW* W = Wd + (size_t)e * d_pad * f_pad;
     for (int t0 = 0; t0 < cnt;) {
       const int r = cnt - t0;
@@ -540,6 +558,7 @@ __device__ __forceinline__ void gateup_mma_items(const __nv_bfloat16* __restrict
     const int a = (int)(item / groups), gi = (int)(item % groups);
     const int e = p.active[a];
     const int cnt = p.counts[e], off = p.offsets[e];
+    if (lane == 0) check_item(p, off, cnt, gi == 0);
     const int feat0 = gi * 8;
     // packed W_gu: per 16 features, 16 gate rows then 16 up rows
     const int rg = (feat0 >> 4) * 32 + (feat0 & 15) + g;
@@ -573,6 +592,7 @@ __device__ __forceinline__ void down_mma_items(const __nv_bfloat16* __restrict__
     const int a = (int)(item / groups), gi = (int)(item % groups);
     const int e = p.active[a];
     const int cnt = p.counts[e], off = p.offsets[e];
+    if (lane == 0) check_item(p, off, cnt, gi == 0);
     const int r0 = gi * 16 + g, r1 = r0 + 8;
     const __nv_bfloat16* W = Wd + (size_t)e * d_pad * f_pad;
     // rows past d_pad (d_pad % 16 == 8) read row d_pad - 1 and are not stored

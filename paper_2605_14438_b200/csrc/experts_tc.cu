@@ -62,6 +62,8 @@ struct Args {
   int apol;         // weight-tile L2 policy (a_policy)
   int epi_skip;     // diagnostics (BEAM_EPI_SKIP=1): TMEM drained but no math / stores
   int epi_direct;   // mode 1: store rows straight from registers (BEAM_EPI_DIRECT=1; default off)
+  int b_rows = 0;   // checked build: rows of the B operand (packed tokens / act)
+  unsigned* check = nullptr;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -593,6 +595,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       uint32_t phase = 0;
       for (int t = u0; t < total; t += ustep) {
         const Tile tl = decode(t, tile_off, E, MG, 2, rank, args);
+#ifdef BEAM_DEVICE_CHECKS
+        if (args.check != nullptr && args.b_rows > 0 && tl.b_row0 + tl.ntok > args.b_rows) atomicOr(args.check, kChkTile);
+#endif
         const uint64_t polA = args.mode == 2 ? polB : a_policy(args.apol, tile_off[tl.e + 1] - tile_off[tl.e] > 1);
         const int half = tl.nmma >> 1;  // token rows staged by each CTA
         const int nbox = (half + kBBox - 1) / kBBox;
@@ -685,12 +690,14 @@ __global__ void __launch_bounds__(256) pack_x_kernel(const TX* __restrict__ h, c
   __syncthreads();
   griddep_wait();
   const int total = min(p.meta[1], cap);
+  BEAM_DCHECK(p, p.meta[1] <= cap, kChkPlanPos);
   const int lane = threadIdx.x & 31;
   constexpr int kL = sizeof(TX) == 2 ? 1 : 2;  // 16-byte loads per 8 elements
   constexpr int kU = sizeof(TX) == 2 ? 8 : 4;  // 8-element chunks per lane in flight
   const bool scale = inv != nullptr || nw != nullptr;
   for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < total; row += gridDim.x * 8) {
     const int tok = p.tok[row];
+    BEAM_DCHECK(p, p.T == 0 || tok < p.T, kChkToken);
     __nv_bfloat16* dst = X + (size_t)row * d_pad;
     if (tok < 0) {
       for (int k = lane * 8; k < d_pad; k += 256) *reinterpret_cast<uint4*>(dst + k) = make_uint4(0, 0, 0, 0);
@@ -910,10 +917,10 @@ cudaError_t launch_experts_tc(const beam_layer_t& L, const Dims& g, const void* 
     const char* v = getenv("BEAM_EPI_SKIP");  // diagnostics only: invalid results
     return v && v[0] == '1' ? 1 : 0;
   }();
-  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN, 0, 0, apol, epi_skip, epi_direct};
+  Args a1{0, g.E, 2 * g.f_pad, g.d_pad, g.d_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN, 0, 0, apol, epi_skip, epi_direct, cap, p.check};
   cudaError_t e = launch_gemm(mA1, mB1, a1, smem, true, s);
   if (e != cudaSuccess) return e;
-  Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN, 0, 0, apol, epi_skip, epi_direct};
+  Args a2{1, g.E, g.d_pad, g.f_pad, g.f_pad / BK, p.counts, p.offsets, p.w, (__nv_bfloat16*)act16, g.f_pad, opair, g.d_pad, BN, 0, 0, apol, epi_skip, epi_direct, cap, p.check};
   return launch_gemm(mA2, mB2, a2, smem, true, s);
 }
 

@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kMcThreads) permute_scatter_kernel(const IdT* 
     const int rank = __popc(peers & ((1u << lane) - 1u));
     if (valid) {
       const int pos = sh[warp * E + e] + rank;
+      BEAM_DCHECK(p, p.cap == 0 || (pos >= 0 && pos < p.cap), kChkPlanPos);
       const int t = i / K;
       p.tok[pos] = t;
       p.slot[pos] = i - t * K;

@@ -425,6 +425,7 @@ __device__ __forceinline__ void permute_block(const IdT* __restrict__ ids, const
     const int rank = __popc(peers & ((1u << lane) - 1u));
     if (valid) {
       const int pos = off_s[e] + hist[warp * E + e] + rank;
+      BEAM_DCHECK(p, p.cap == 0 || (pos >= 0 && pos < p.cap), kChkPlanPos);
       const int t = i / K;
       p.tok[pos] = t;
       p.slot[pos] = i - t * K;
@@ -590,6 +591,7 @@ __device__ __forceinline__ void plan_warp(const int32_t* ids, const float* w, in
   }
   if (valid) {
     const int pos = before + within;
+    BEAM_DCHECK(p, p.cap == 0 || (pos >= 0 && pos < p.cap), kChkPlanPos);
     const int t = lane / K;
     p.tok[pos] = t;
     p.slot[pos] = lane - t * K;
