@@ -353,8 +353,21 @@ def algorithmic_bytes(t, s_real, e_act, r, d, f, n, k=Q30["k"], wbytes=2, xbytes
     return w_exp + w_gate + act + meta
 
 
+def gateup_kernel_name(t, r, e_act, f, sms=148):
+    """Which gate/up kernel runs the expert stage (the device-side rule of
+    experts_simt.cu: CTA items at T <= 2; tensor-core items when active experts
+    average >= 2 surviving tokens and give every warp >= 3 items)."""
+    if t <= 2:
+        return "gateup_cta_kernel"
+    f_pad = (f + 15) // 16 * 16
+    mma = r >= 2 * e_act and e_act * (f_pad // 8) >= 3 * 2 * sms * 8
+    return "gateup_mma_kernel" if mma else "gateup_ffma_kernel"
+
+
 def gateup_bytes(t, e_act, r, d, f):
-    return e_act * 2 * f * d * 2 + t * d * 2 + r * f * 4
+    """Algorithmic bytes of the gate/up stage: the active experts' gate + up
+    rows (bf16), one read of the token rows, the bf16 act rows written."""
+    return e_act * 2 * f * d * 2 + t * d * 2 + r * f * 2
 
 
 def timed_steps(layer, steps, flush, use_graph=True):
@@ -566,7 +579,7 @@ def run_ours(args):
     names = ("gate", "permute", "experts_gateup", "experts_down", "combine")
     stage_us = {nm: stage[i] * 1e3 / max(ncalls.value, 1) for i, nm in enumerate(names)}
     gu_bytes = gateup_bytes(t, pt["e_act"], pt["r"], d, f)
-    dn_bytes = pt["e_act"] * d * f * 2 + pt["r"] * f * 4 + pt["r"] * d * 4
+    dn_bytes = pt["e_act"] * d * f * 2 + pt["r"] * f * 2 + pt["r"] * d * 4  # W_down + bf16 act in + fp32 rows out
     gu_gbs = gu_bytes / (stage_us["experts_gateup"] * 1e-6) / 1e9
     layer_bytes = algorithmic_bytes(t, pt["s_real"], pt["e_act"], pt["r"], d, f, n)
 
@@ -687,11 +700,11 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": t * d * 2,
                 "d2h_bytes_per_step": probe.nbytes,
                 "path": "paper_2605_14438_b200.beam_block_forward(pinned host h) -> host outputs"},
-        "roofline": {"bound": "hbm", "kernel": "gateup_kernel (experts gate/up, weight streaming)",
+        "roofline": {"bound": "hbm", "kernel": gateup_kernel_name(t, pt["r"], pt["e_act"], f) + " (experts gate/up, weight streaming)",
                      "achieved": gu_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gu_gbs / hbm_peak,
                      "frac_of_8tbs": gu_gbs / 8000.0,
                      "peak_kind": peak_kind + " (copy bandwidth, MEASURED_PEAKS.json hbm_gbs)",
-                     "traffic": ncu_traffic("gateup_ffma_kernel" if t > 2 else "gateup_cta_kernel", f"T={t} s={s}"),
+                     "traffic": ncu_traffic(gateup_kernel_name(t, pt["r"], pt["e_act"], f), f"T={t} s={s}"),
                      "algorithmic_bytes_per_launch": gu_bytes,
                      "layer": {"bytes": layer_bytes, "achieved_gbs": layer_bytes / (ms * 1e-3) / 1e9,
                                "frac": layer_bytes / (ms * 1e-3) / 1e9 / hbm_peak},

@@ -6,7 +6,7 @@ mkdir -p gpurun_out/r02
 B="python bench.py --steps 3 --warmup 3 --no-sweep --no-cpu --no-train --no-shapes"
 K='regex:gate_fused|router_gemv|topk_mask|permute|gateup|down_|combine|pack_x|grouped_gemm'
 $B --tokens 64 > gpurun_out/r02/plain64.log 2>&1 || { echo plain-failed; exit 1; }
-for spec in "64 0.5" "1 0.875" "1 0" "8192 0"; do
+for spec in "64 0.5" "64 0" "1 0.875" "1 0" "8192 0"; do
   set -- $spec
   ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
       --log-file gpurun_out/r02/launches_T$1_s$2.csv $B --tokens $1 --sparsity $2 > /dev/null 2>&1; echo "launches T=$1 s=$2 rc=$?"
@@ -20,5 +20,5 @@ full() {  # tokens sparsity skip count
 full 64 0.5 12 6
 full 64 0 12 6
 full 1 0.875 8 5
-full 8192 0 14 7
+full 8192 0 14 9
 cp profiles/ncu_summary.json gpurun_out/r02/ncu_summary.json
