@@ -12,9 +12,11 @@ import os
 from .tensor import ContractError, ShapeError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-# BEAM_LIB=checked loads the device-checked build (bounds assertions, tests only)
-LIB_PATH = os.path.join(_PKG, "_lib", "libbeam_b200_checked.so" if os.environ.get("BEAM_LIB") == "checked"
-                        else "libbeam_b200.so")
+# BEAM_LIB=checked loads the device-checked build (bounds assertions, tests
+# only); an absolute path loads that file (A/B timing of two builds)
+_SEL = os.environ.get("BEAM_LIB", "")
+LIB_PATH = (_SEL if os.path.isabs(_SEL) else
+            os.path.join(_PKG, "_lib", "libbeam_b200_checked.so" if _SEL == "checked" else "libbeam_b200.so"))
 
 BEAM_OK = 0
 BEAM_ERR_ARG = -1
