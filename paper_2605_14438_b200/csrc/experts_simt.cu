@@ -667,6 +667,53 @@ __global__ void __launch_bounds__(kThreads, 2) gateup_ffma_kernel(const __nv_bfl
     gateup_warp_items<__nv_bfloat16, TX, ACT>(Wgu, X, inv, nw, d, d_pad, f_pad, p, act, red_s);
 }
 
+// One launch for both item kinds (the device picks from the plan): the FFMA body
+// is a separate, non-inlined function so the kernel's register allocation is the
+// larger body's, not their sum (inlined together they spill); the tensor-core
+// body stays inline (as a call it lost 4-8 %).
+template <typename TX, int ACT>
+__device__ __forceinline__ void gateup_mma_body(const __nv_bfloat16* __restrict__ Wgu, const TX* __restrict__ X,
+                                             const float* __restrict__ inv, int d_pad, int f_pad, PlanDev p,
+                                             __nv_bfloat16* __restrict__ act) {
+  gateup_mma_items<TX, ACT>(Wgu, X, inv, d_pad, f_pad, p, act);
+}
+template <typename TX, int ACT>
+__device__ __noinline__ void gateup_ffma_body(const __nv_bfloat16* __restrict__ Wgu, const TX* __restrict__ X,
+                                              const float* __restrict__ inv, const float* __restrict__ nw, int d,
+                                              int d_pad, int f_pad, PlanDev p, __nv_bfloat16* __restrict__ act) {
+  __shared__ float red_s[kWarps][32];
+  gateup_warp_items<__nv_bfloat16, TX, ACT>(Wgu, X, inv, nw, d, d_pad, f_pad, p, act, red_s);
+}
+template <typename TXM, typename TXF, int ACT>
+__global__ void __launch_bounds__(kThreads, 2) gateup_mix_kernel(const __nv_bfloat16* __restrict__ Wgu,
+                                                                 const TXM* __restrict__ Xm,
+                                                                 const TXF* __restrict__ Xf,
+                                                                 const float* __restrict__ inv,
+                                                                 const float* __restrict__ nw, int d, int d_pad,
+                                                                 int f_pad, PlanDev p,
+                                                                 __nv_bfloat16* __restrict__ act, int tok) {
+  griddep_wait();
+  if (use_mma_items(p, f_pad / 8, tok)) gateup_mma_body<TXM, ACT>(Wgu, Xm, inv, d_pad, f_pad, p, act);
+  else gateup_ffma_body<TXF, ACT>(Wgu, Xf, inv, nw, d, d_pad, f_pad, p, act);
+}
+
+__device__ __forceinline__ void down_mma_body(const __nv_bfloat16* __restrict__ Wd, const __nv_bfloat16* __restrict__ act,
+                                           int d_pad, int f_pad, PlanDev p, float* __restrict__ opair) {
+  down_mma_items(Wd, act, d_pad, f_pad, p, opair);
+}
+__device__ __noinline__ void down_ffma_body(const __nv_bfloat16* __restrict__ Wd, const __nv_bfloat16* __restrict__ act,
+                                            int d_pad, int f_pad, PlanDev p, float* __restrict__ opair) {
+  __shared__ float red_s[kWarps][32];
+  down_warp_items<__nv_bfloat16>(Wd, act, d_pad, f_pad, p, opair, red_s);
+}
+__global__ void __launch_bounds__(kThreads, 2) down_mix_kernel(const __nv_bfloat16* __restrict__ Wd,
+                                                               const __nv_bfloat16* __restrict__ act, int d_pad,
+                                                               int f_pad, PlanDev p, float* __restrict__ opair, int tok) {
+  griddep_wait();
+  if (use_mma_items(p, (d_pad + 15) / 16, tok)) down_mma_body(Wd, act, d_pad, f_pad, p, opair);
+  else down_ffma_body(Wd, act, d_pad, f_pad, p, opair);
+}
+
 __global__ void __launch_bounds__(kThreads, 2) down_mma_kernel(const __nv_bfloat16* __restrict__ Wd,
                                                                const __nv_bfloat16* __restrict__ act, int d_pad,
                                                                int f_pad, PlanDev p, float* __restrict__ opair, int tok) {
@@ -720,16 +767,22 @@ static void gateup_dispatch(const beam_layer_t& L, const Dims& g, const void* X,
       // tensor-core items read the bf16 copy of the rows when there is one
       // (one MMA pair per step instead of the fp32 hi + lo pairs)
       const bool b16 = X16 != nullptr;
-      if (L.activation == BEAM_ACT_SILU) {
-        if (mma && b16) launch_pdl(gateup_mma_kernel<__nv_bfloat16, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const __nv_bfloat16*)X16, inv, g.d_pad, g.f_pad, p, act, tok);
-        else if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act, tok);
-        launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act, tok);
+      if (!mma) {  // the tensor-core items are ruled out from the slot count
+        if (L.activation == BEAM_ACT_SILU)
+          launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act, tok);
+        else
+          launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act, tok);
+      } else if (b16) {  // one launch, item kind picked on the device
+        if (L.activation == BEAM_ACT_SILU)
+          launch_pdl(gateup_mix_kernel<__nv_bfloat16, TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const __nv_bfloat16*)X16, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act, tok);
+        else
+          launch_pdl(gateup_mix_kernel<__nv_bfloat16, TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const __nv_bfloat16*)X16, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act, tok);
       } else {
-        if (mma && b16) launch_pdl(gateup_mma_kernel<__nv_bfloat16, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const __nv_bfloat16*)X16, inv, g.d_pad, g.f_pad, p, act, tok);
-        else if (mma) launch_pdl(gateup_mma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, g.d_pad, g.f_pad, p, act, tok);
-        launch_pdl(gateup_ffma_kernel<TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act, tok);
+        if (L.activation == BEAM_ACT_SILU)
+          launch_pdl(gateup_mix_kernel<TX, TX, BEAM_ACT_SILU>, grid, kThreads, 0, s, W, (const TX*)X, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act, tok);
+        else
+          launch_pdl(gateup_mix_kernel<TX, TX, BEAM_ACT_IDENTITY>, grid, kThreads, 0, s, W, (const TX*)X, (const TX*)X, inv, nw, g.d, g.d_pad, g.f_pad, p, act, tok);
       }
-      if (mma) count_launches(1);
     }
   } else {
     if (L.activation == BEAM_ACT_SILU)
@@ -770,9 +823,8 @@ cudaError_t launch_down_simt(const beam_layer_t& L, const Dims& g, int T, const 
     else if (mma_enabled()) {
       const int tok = mma_tok(1);
       const bool mma = mma_possible(slots, (g.d_pad + 15) / 16, tok, grid);
-      if (mma) launch_pdl(down_mma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair, tok);
-      launch_pdl(down_ffma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair, tok);
-      if (mma) count_launches(1);
+      if (mma) launch_pdl(down_mix_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair, tok);
+      else launch_pdl(down_ffma_kernel, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair, tok);
     }
     else launch_pdl(down_warp_kernel<__nv_bfloat16>, grid, kThreads, 0, s, (const __nv_bfloat16*)L.w_down, (const __nv_bfloat16*)act, g.d_pad, g.f_pad, p, opair);
   } else {
