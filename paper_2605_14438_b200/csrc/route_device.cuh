@@ -251,6 +251,30 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
       ss += sp < splits ? v : 0.0f;
     }
     inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
+  } else if (!CG && a.has_norm && a.xw_out == nullptr) {  // tensor.py:485-487, prefill (no prescaled rows)
+    // 16-byte loads, a batch of XU in flight per lane (8-byte loads 8 deep waited
+    // twice as many dependent round trips per row: top-K at T = 8192 37 -> 25 us)
+    constexpr int EPL = 16 / (int)sizeof(TX);
+    constexpr int XU = 4;
+    const TX* row = X + (size_t)t * a.d_pad;
+    float ss = 0.0f;
+    for (int k0 = EPL * lane; k0 < a.d_pad; k0 += 32 * EPL * XU) {
+      uint4 r[XU];
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        const int k = k0 + 32 * EPL * u;
+        r[u] = k < a.d_pad ? ld_cached(row + k) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        float f[EPL];
+        unpack<TX>(r[u], f);
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) ss = fmaf(f[e], f[e], ss);
+      }
+    }
+    ss = warp_sum(ss);
+    inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
   } else if (a.has_norm) {  // tensor.py:485-487: (mean(x^2) + eps)^-1/2 over the real d entries
     const TX* row = X + (size_t)t * a.d_pad;
     float* xw = a.xw_out != nullptr ? a.xw_out + (size_t)t * a.d_pad : nullptr;
