@@ -353,15 +353,16 @@ def algorithmic_bytes(t, s_real, e_act, r, d, f, n, k=Q30["k"], wbytes=2, xbytes
     return w_exp + w_gate + act + meta
 
 
-def gateup_kernel_name(t, r, e_act, f, sms=148):
-    """Which gate/up kernel runs the expert stage (the device-side rule of
-    experts_simt.cu: CTA items at T <= 2; tensor-core items when active experts
-    average >= 2 surviving tokens and give every warp >= 3 items)."""
+def gateup_kernel_name(t, r, e_act, f, sms=148, k=8):
+    """Which gate/up kernel runs the expert stage (the host-side rule of
+    experts_simt.cu: CTA items at T <= 2; the one-launch tensor-core / FFMA item
+    kernel when the planned slots T*K could give every warp >= 3 tensor-core
+    items (mma_possible) — the device then picks the item kind — else FFMA only)."""
     if t <= 2:
         return "gateup_cta_kernel"
     f_pad = (f + 15) // 16 * 16
-    mma = r >= 2 * e_act and e_act * (f_pad // 8) >= 3 * 2 * sms * 8
-    return "gateup_mma_kernel" if mma else "gateup_ffma_kernel"
+    e_min = -(-3 * 2 * sms * 8 // (f_pad // 8))
+    return "gateup_mix_kernel" if t * k >= 2 * e_min else "gateup_ffma_kernel"
 
 
 def gateup_bytes(t, e_act, r, d, f):
@@ -375,8 +376,11 @@ def timed_steps(layer, steps, flush, use_graph=True):
     import torch
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    rsweep = os.environ.get("BEAM_BENCH_FLUSH") == "rw"  # diagnostics: memset, then a read sweep (clean L2)
     for s_ev, e_ev in evs:
         flush.zero_()
+        if rsweep:
+            flush[: 256 << 20].view(torch.int32).sum()
         s_ev.record()
         layer.replay() if use_graph else layer.eager()
         e_ev.record()
