@@ -13,7 +13,7 @@
 // (8 x 16-byte L1-bypassing loads per thread) and small batches are latency-, not
 // issue-bound.  Partial dot products are reduced with a warp transpose-reduce
 // butterfly, then across warps through shared memory in a fixed order
-// (deterministic, independent of the grid).  Two launches:
+// (deterministic, independent of the grid).  Two stages:
 //   gateup: 4 gate + 4 up rows per item -> act[pos, f] = act(g) * u   (fp32)
 //   down:   2 x 8 output rows per item  -> opair[pos, d] = ghat * (act . W_down)
 #include <cstdlib>
@@ -639,19 +639,9 @@ static int mma_tok(int which) {
   return v[which];
 }
 
-// Two launches per stage, each leaving at once when the plan picks the other
-// (one kernel holding both bodies spills, or with 2-token FFMA passes runs the
-// FFMA items up to 15 % slower): MMA items first, then the FFMA items.  The host
-// skips the MMA launch when T * Keff rules it out (mma_possible).
-template <typename TX, int ACT>
-__global__ void __launch_bounds__(kThreads, 2) gateup_mma_kernel(const __nv_bfloat16* __restrict__ Wgu,
-                                                                 const TX* __restrict__ X,
-                                                                 const float* __restrict__ inv, int d_pad,
-                                                                 int f_pad, PlanDev p, __nv_bfloat16* __restrict__ act,
-                                                                 int tok) {
-  griddep_wait();
-  if (use_mma_items(p, f_pad / 8, tok)) gateup_mma_items<TX, ACT>(Wgu, X, inv, d_pad, f_pad, p, act);
-}
+// FFMA-only launch: the host picks it when T * Keff rules the tensor-core items
+// out (mma_possible); otherwise the one-launch mix kernels below run, and the
+// device picks the item kind from the plan.
 template <typename TX, int ACT>
 __global__ void __launch_bounds__(kThreads, 2) gateup_ffma_kernel(const __nv_bfloat16* __restrict__ Wgu,
                                                                   const TX* __restrict__ X,
@@ -714,12 +704,6 @@ __global__ void __launch_bounds__(kThreads, 2) down_mix_kernel(const __nv_bfloat
   else down_ffma_body(Wd, act, d_pad, f_pad, p, opair);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) down_mma_kernel(const __nv_bfloat16* __restrict__ Wd,
-                                                               const __nv_bfloat16* __restrict__ act, int d_pad,
-                                                               int f_pad, PlanDev p, float* __restrict__ opair, int tok) {
-  griddep_wait();
-  if (use_mma_items(p, (d_pad + 15) / 16, tok)) down_mma_items(Wd, act, d_pad, f_pad, p, opair);
-}
 __global__ void __launch_bounds__(kThreads, 2) down_ffma_kernel(const __nv_bfloat16* __restrict__ Wd,
                                                                 const __nv_bfloat16* __restrict__ act, int d_pad,
                                                                 int f_pad, PlanDev p, float* __restrict__ opair, int tok) {
