@@ -16,9 +16,11 @@ front.  ``mask_forward`` alone honours any tau via a >= logit(tau).
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import functools
 import math
+import os
 import threading
 from dataclasses import dataclass
 
@@ -233,6 +235,53 @@ def layer_forward_into(x: torch.Tensor, block: MoEBlock, outs: LayerOutputs,
                "beam_layer_forward")
 
 
+class _HostSession:
+    """Host-buffer fast path of beam_block_forward for one (block, T, dtype,
+    block_size): fixed device rows / outputs and the layer's kernels captured
+    ONCE as a CUDA graph (workspace of a private stream).  A call is then: H2D of
+    the rows, one graph launch, one D2H of all outputs into fresh pinned memory —
+    the per-call host work is a few microseconds instead of the eager launch
+    sequence (~35 us of Python + ctypes + 4-5 kernel launches)."""
+
+    def __init__(self, block: MoEBlock, t: int, dtype: torch.dtype, block_size: int, dev: torch.device):
+        cfg = block.cfg
+        self.lock = threading.Lock()
+        self.x = torch.zeros(t, cfg.d_h, dtype=dtype, device=dev)
+        self.outs = LayerOutputs(t, cfg.d_h, cfg.num_experts, cfg.top_k, dtype, dev)
+        self.stream = torch.cuda.Stream(dev)
+        self.stream.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(self.stream):
+            layer_forward_into(self.x, block, self.outs, block_size)  # sizes this stream's workspace
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            layer_forward_into(self.x, block, self.outs, block_size)
+
+
+_SESSIONS: "collections.OrderedDict" = collections.OrderedDict()
+_SESSIONS_LOCK = threading.Lock()
+_MAX_SESSIONS = 16
+
+
+def _host_session(block: MoEBlock, t: int, dtype: torch.dtype, block_size: int, dev: torch.device):
+    key = (id(block), t, dtype, block_size, dev.index, _EXPERT_PATH[0])
+    with _SESSIONS_LOCK:
+        sess = _SESSIONS.get(key)
+        if sess is not None and sess[0] is block:
+            _SESSIONS.move_to_end(key)
+            return sess[1]
+    new = _HostSession(block, t, dtype, block_size, dev)
+    with _SESSIONS_LOCK:
+        _SESSIONS[key] = (block, new)
+        while len(_SESSIONS) > _MAX_SESSIONS:
+            _SESSIONS.popitem(last=False)
+    return new
+
+
+def _graph_host_path() -> bool:
+    return os.environ.get("BEAM_HOST_GRAPH", "1") != "0"
+
+
 def beam_block_forward(h, block: MoEBlock, training: bool = True, block_size: int = 16):
     """beam.py:127-165 -> (h', RouterDecision, MaskDecision).
 
@@ -252,9 +301,21 @@ def beam_block_forward(h, block: MoEBlock, training: bool = True, block_size: in
         x = x.to(torch.float32)
     host = not x.is_cuda
     dev = block.device
-    xd = x.to(dev, non_blocking=True).contiguous() if host else x.contiguous()
     cfg = block.cfg
-    t = xd.shape[0]
+    t = x.shape[0]
+    if host and t > 0 and _graph_host_path():
+        block.layer_desc(0.0)  # re-packs changed router weights in place (the graph reads those buffers)
+        sess = _host_session(block, t, x.dtype, block_size, dev)
+        with sess.lock:
+            main = torch.cuda.current_stream(dev)
+            sess.x.copy_(x, non_blocking=True)
+            sess.graph.replay()
+            hb = LayerOutputs(t, cfg.d_h, cfg.num_experts, cfg.top_k, x.dtype, "cpu", pin=True)
+            hb.buf.copy_(sess.outs.buf, non_blocking=True)
+            res = _results(hb)  # views built while the GPU works
+            main.synchronize()
+        return res
+    xd = x.to(dev, non_blocking=True).contiguous() if host else x.contiguous()
     outs = LayerOutputs(t, cfg.d_h, cfg.num_experts, cfg.top_k, xd.dtype, dev)
     if host and t > 0:
         # decisions leave the GPU on a side stream while the experts run; `out`

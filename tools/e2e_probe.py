@@ -1,61 +1,60 @@
-"""Where does the host-API time go?  Breaks beam_block_forward(pinned host h)
-into its pieces at the bench headline workload (Q30, T=64, s=0.5)."""
+"""Public-API latency with host buffers (bench.py's e2e measure) at the headline
+workload, eager launch path vs the cached-CUDA-graph host path
+(BEAM_HOST_GRAPH=0 / 1), plus the outputs of both compared bit for bit.
+    python tools/e2e_probe.py"""
+import os
+import subprocess
+import sys
 import time
 
-import os
-import sys
-
 import numpy as np
-import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-
-import paper_2605_14438_b200 as B
-from paper_2605_14438_b200.beam import LayerOutputs, layer_forward_into
-
-import bench
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def wall(fn, n=50):
-    for _ in range(5):
-        fn()
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(n):
-        t0 = time.perf_counter()
-        fn()
-        ts.append((time.perf_counter() - t0) * 1e6)
-    return float(np.median(ts))
-
-
-def main():
+def run():
+    import torch
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2605_14438_b200 as B
     dev = torch.device("cuda", 0)
-    Q = bench.Q30
-    cfg = B.MoEBlockConfig(d_h=Q["d"], d_ff=Q["f"], num_experts=Q["n"], top_k=Q["k"])
+    q = bench.Q30
+    cfg = B.MoEBlockConfig(d_h=q["d"], d_ff=q["f"], num_experts=q["n"], top_k=q["k"])
     w = bench.make_layer0()
-    blk = B.MoEBlock.from_weights(cfg, w["router"], (w["wg"], w["wu"], w["wd"]), norm_w=None,
-                                  mask_w=w["mask"], dtype=torch.bfloat16, device=dev)
-    hc = bench.make_tokens(64, 7)
-    theta = bench.calibrate_theta(hc, w["router"], w["mask"], Q["k"], 0.5)
-    blk.mask_router.weight.copy_(bench.mask_with_theta(w["mask"], theta).to(dev))
-    h = hc.to(dev)
-    h_pin = hc.pin_memory()
-    t, d = h.shape
-    outs = LayerOutputs(t, d, cfg.num_experts, cfg.top_k, h.dtype, h.device)
+    blk = B.MoEBlock.from_weights(cfg, w["router"], (w["wg"], w["wu"], w["wd"]), mask_w=w["mask"],
+                                  dtype=torch.bfloat16, device=dev)
     res = {}
-    res["desc_us"] = wall(lambda: blk.layer_desc(0.0))
-    res["outs_alloc_dev_us"] = wall(lambda: LayerOutputs(t, d, cfg.num_experts, cfg.top_k, h.dtype, h.device))
-    res["outs_alloc_pin_us"] = wall(lambda: LayerOutputs(t, d, cfg.num_experts, cfg.top_k, h.dtype, "cpu", pin=True))
-    res["h2d_sync_us"] = wall(lambda: (h_pin.to("cuda", non_blocking=True), torch.cuda.synchronize()))
-    res["launch_only_us"] = wall(lambda: layer_forward_into(h, blk, outs))
-    torch.cuda.synchronize()
-    res["layer_sync_us"] = wall(lambda: (layer_forward_into(h, blk, outs), torch.cuda.synchronize()))
-    hb = LayerOutputs(t, d, cfg.num_experts, cfg.top_k, h.dtype, "cpu", pin=True)
-    res["d2h_sync_us"] = wall(lambda: (hb.copy_from(outs), torch.cuda.synchronize()))
-    res["public_api_us"] = wall(lambda: B.beam_block_forward(h_pin, blk, training=False))
-    res["public_api_dev_input_us"] = wall(lambda: (B.beam_block_forward(h, blk, training=False), torch.cuda.synchronize()))
-    print(res)
+    for t in (1, 64):
+        h = bench.make_tokens(t, 7)
+        theta = bench.calibrate_theta(h, w["router"], w["mask"], q["k"], 0.5)
+        blk.mask_router.weight.copy_(bench.mask_with_theta(w["mask"], theta).to(dev))
+        hp = h.pin_memory()
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        for _ in range(10):
+            B.beam_block_forward(hp, blk, training=False)
+        ts = []
+        for _ in range(50):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out, dec, md = B.beam_block_forward(hp, blk, training=False)
+            ts.append(time.perf_counter() - t0)
+        print(f"T={t} graph={os.environ.get('BEAM_HOST_GRAPH', '1')}: e2e mean {np.mean(ts) * 1e6:.1f} us, "
+              f"min {np.min(ts) * 1e6:.1f} us -> {t / np.mean(ts):.0f} tok/s", flush=True)
+        res[f"T{t}_out"] = out.float().numpy()
+        res[f"T{t}_ids"] = dec.topk_indices.numpy()
+        res[f"T{t}_mask"] = md.mask.numpy()
+        res[f"T{t}_logits"] = dec.logits.numpy()
+    np.savez(sys.argv[2], **res)
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--run":
+        run()
+    else:
+        os.makedirs("/tmp/e2e", exist_ok=True)
+        for g in ("0", "1"):
+            subprocess.run([sys.executable, __file__, "--run", f"/tmp/e2e/g{g}.npz"], env={**os.environ, "BEAM_HOST_GRAPH": g},
+                           check=True)
+        a, b = np.load("/tmp/e2e/g0.npz"), np.load("/tmp/e2e/g1.npz")
+        print("outputs identical:", all(np.array_equal(a[k], b[k]) for k in a.files))
