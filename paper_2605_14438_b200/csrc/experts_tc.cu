@@ -695,8 +695,14 @@ __global__ void __launch_bounds__(256) pack_x_kernel(const TX* __restrict__ h, c
   constexpr int kL = sizeof(TX) == 2 ? 1 : 2;  // 16-byte loads per 8 elements
   constexpr int kU = sizeof(TX) == 2 ? 8 : 4;  // 8-element chunks per lane in flight
   const bool scale = inv != nullptr || nw != nullptr;
-  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < total; row += gridDim.x * 8) {
-    const int tok = p.tok[row];
+  const int stride = gridDim.x * 8;
+  int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  int tok_next = row < total ? p.tok[row] : -1;
+  for (; row < total; row += stride) {
+    // the next row's token index is in flight while this row is copied (one
+    // dependent L2 round trip per row instead of two)
+    const int tok = tok_next;
+    tok_next = row + stride < total ? p.tok[row + stride] : -1;
     BEAM_DCHECK(p, p.T == 0 || tok < p.T, kChkToken);
     __nv_bfloat16* dst = X + (size_t)row * d_pad;
     if (tok < 0) {
@@ -806,7 +812,18 @@ bool tc_supported(const beam_layer_t& L, const Dims& g) {
 
 cudaError_t launch_pack_x(const void* h, int h_dtype, const float* inv, const float* nw, const Dims& g,
                           const PlanDev& p, int cap, void* xperm, cudaStream_t s) {
-  const int grid = std::max(1, std::min(num_sms() * 8, (cap + 7) / 8));
+  // one resident wave (grid-stride rows): a grid sized for 8 CTAs / SM ran in
+  // ~2.7 waves at the kernel's 3 resident CTAs / SM
+  static int resident[2] = {0, 0};
+  int& nb = resident[h_dtype == BEAM_BF16 ? 0 : 1];
+  if (nb == 0) {
+    if (h_dtype == BEAM_BF16)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tc::pack_x_kernel<__nv_bfloat16>, 256, g.d_pad * sizeof(float));
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tc::pack_x_kernel<float>, 256, g.d_pad * sizeof(float));
+    nb = std::max(nb, 1);
+  }
+  const int grid = std::max(1, std::min(num_sms() * nb, (cap + 7) / 8));
   if (h_dtype == BEAM_BF16)
     launch_pdl(tc::pack_x_kernel<__nv_bfloat16>, grid, 256, g.d_pad * sizeof(float), s, (const __nv_bfloat16*)h, inv, nw, g.d, g.d_pad, p, cap, (__nv_bfloat16*)xperm);
   else
