@@ -46,10 +46,15 @@ __device__ __forceinline__ void chunk_hist(const IdT* __restrict__ ids, int M, i
   __syncthreads();
   const int begin = blockIdx.x * kMcChunk + warp * kMcPerWarp;
   const int end = min(M, begin + kMcPerWarp);
-  for (int i = begin + lane; i < end; i += 32) {
-    const long long e = (long long)ids[i];
-    if (e >= 0 && e < E) atomicAdd(&sh[warp * E + (int)e], 1);
+  long long ev[kMcPerWarp / 32];  // all of the warp's ids in flight at once
+#pragma unroll
+  for (int j = 0; j < kMcPerWarp / 32; ++j) {
+    const int i = begin + lane + 32 * j;
+    ev[j] = i < end ? (long long)ids[i] : -1;
   }
+#pragma unroll
+  for (int j = 0; j < kMcPerWarp / 32; ++j)
+    if (ev[j] >= 0 && ev[j] < E) atomicAdd(&sh[warp * E + (int)ev[j]], 1);
   __syncthreads();
 }
 
@@ -84,12 +89,12 @@ __global__ void __launch_bounds__(kMcThreads) permute_hist_kernel(const IdT* __r
     int run = 0;
     if (e < E) {
       int q = 0;
-      for (; q + 8 <= G; q += 8) {  // 8 independent loads per round
-        int c[8];
+      for (; q + 32 <= G; q += 32) {  // 32 independent loads per round
+        int c[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) c[u] = __ldcg(hist_g + (size_t)(q + u) * E + e);
+        for (int u = 0; u < 32; ++u) c[u] = __ldcg(hist_g + (size_t)(q + u) * E + e);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 32; ++u) {
           hist_g[(size_t)(q + u) * E + e] = run;
           run += c[u];
         }
@@ -147,10 +152,19 @@ __global__ void __launch_bounds__(kMcThreads) permute_scatter_kernel(const IdT* 
   __syncthreads();
   const int begin = blockIdx.x * kMcChunk + warp * kMcPerWarp;
   const int end = min(M, begin + kMcPerWarp);
-  for (int b0 = begin; b0 < end; b0 += 32) {
-    const int i = b0 + lane;
-    long long e = -1;
-    if (i < end) e = (long long)ids[i];
+  long long ev[kMcPerWarp / 32];  // the warp's ids and weights loaded once, all in flight
+  float wv[kMcPerWarp / 32];
+#pragma unroll
+  for (int j = 0; j < kMcPerWarp / 32; ++j) {
+    const int i = begin + lane + 32 * j;
+    ev[j] = i < end ? (long long)ids[i] : -1;
+    wv[j] = i < end && w != nullptr ? w[i] : 0.0f;
+  }
+#pragma unroll
+  for (int j = 0; j < kMcPerWarp / 32; ++j) {
+    const int i = begin + 32 * j + lane;
+    if (begin + 32 * j >= end) break;
+    const long long e = ev[j];
     const bool valid = i < end && e >= 0 && e < E;
     const int key = valid ? (int)e : (E + lane);
     const unsigned peers = __match_any_sync(0xffffffffu, key);
@@ -161,7 +175,7 @@ __global__ void __launch_bounds__(kMcThreads) permute_scatter_kernel(const IdT* 
       const int t = i / K;
       p.tok[pos] = t;
       p.slot[pos] = i - t * K;
-      if (p.w) p.w[pos] = w ? w[i] : 0.0f;
+      if (p.w) p.w[pos] = wv[j];
       if (p.slot_pos) p.slot_pos[i] = pos;
       if (p.slot_expert) p.slot_expert[i] = (int)e;
     } else if (i < end) {
