@@ -85,11 +85,13 @@ __device__ __forceinline__ void topk_finish(float (&v)[NPL], float (&av)[NPL], f
     unsigned long long best = key[0];
 #pragma unroll
     for (int i = 1; i < NPL; ++i) best = key[i] > best ? key[i] : best;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
-      best = other > best ? other : best;
-    }
+    // warp max of the 64-bit keys as two 32-bit redux.sync reductions (value
+    // order first, then the lowest column among equal values): 2 instructions
+    // instead of a 5-level butterfly of 64-bit shuffles
+    const unsigned bhi = (unsigned)(best >> 32), blo = (unsigned)best;
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, bhi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, bhi == mhi ? blo : 0u);
+    best = ((unsigned long long)mhi << 32) | mlo;
     const int bj = (int)(~(unsigned)(best & 0xffffffffull));
     if (r == 0) top_j = bj;
 #pragma unroll
