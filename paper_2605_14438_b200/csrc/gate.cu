@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(const TX* __restrict__ 
   TopkArgs b = a;
   b.ss_part = ssp;
   b.trace = g_gate_trace;
-  int* scratch = reinterpret_cast<int*>(xs);  // plan_warp: [0, 64 + E), E <= 256
+  int* scratch = reinterpret_cast<int*>(xs);  // plan_warp: [0, 3 E) (reads ids_s / gw_s before writing there)
   if (one_warp_plan) {
     b.ids_s = scratch + 320;
     b.gw_s = reinterpret_cast<float*>(scratch + 352);

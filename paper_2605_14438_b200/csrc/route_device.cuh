@@ -576,18 +576,18 @@ __device__ __forceinline__ void plan_small_block(const int32_t* ids, const float
 // The plan of at most 32 (token, slot) entries by ONE warp (decode, T * Keff <=
 // 32): lane i holds entry i; same-expert lanes find each other with match_any
 // (a lane's rank among them = its position inside the expert's run, ascending
-// flat index), the experts' runs are ordered by expert id through a 32-entry
-// table in shared memory; the offsets of all E experts come from one warp scan
-// over a padded-count table the leaders scatter into.  Same outputs as
-// permute_block, no CTA barrier.  ids / w may live in shared memory (the fused
-// gate hands them over from its top-K warps without an L2 round trip).
-// smem: 2 * 32 + E ints.
+// flat index); the leaders scatter their padded counts into a per-expert table,
+// one warp scan over it gives every expert's offset AND active index (the
+// leaders read theirs back), so a run's start needs no search over the other
+// leaders.  Same outputs as permute_block, no CTA barrier.  ids / w may live in
+// shared memory (the fused gate hands them over from its top-K warps without an
+// L2 round trip).  smem: 3 * E ints.
 template <bool CG>
 __device__ __forceinline__ void plan_warp(const int32_t* ids, const float* w, int T, int K, int E, int bs,
                                           const PlanDev& p, bool pad, int lane, int* smem) {
-  int* le = smem;       // [32] leader experts (INT_MAX = none)
-  int* lp = smem + 32;  // [32] padded counts
-  int* tab = smem + 64; // [E] padded count per expert (0 = inactive)
+  int* tab = smem;          // [E] padded count per expert (0 = inactive)
+  int* offs = smem + E;     // [E] exclusive scan of tab
+  int* aidx = smem + 2 * E; // [E] number of active experts below e
   const int M = T * K;
   int e = -1;
   float wi = 0.0f;
@@ -602,21 +602,45 @@ __device__ __forceinline__ void plan_warp(const int32_t* ids, const float* w, in
   const int cnt = __popc(peers);
   const bool leader = valid && within == 0;
   const int padded = leader ? round_up(cnt, bs) : 0;
-  le[lane] = leader ? e : 0x7fffffff;
-  lp[lane] = padded;
   __syncwarp();
   if (leader) tab[e] = padded;
-  int before = 0, act_before = 0;
-#pragma unroll 8
-  for (int j = 0; j < 32; ++j) {
-    const int ej = le[j];
-    if (ej < e) {
-      before += lp[j];
-      ++act_before;
+  const int n_act = __popc(__ballot_sync(0xffffffffu, leader));
+  const int n_real = __popc(__ballot_sync(0xffffffffu, valid));
+  __syncwarp();
+  // counts / padded offsets / active indices of every expert (inactive: count 0):
+  // lane l owns the contiguous experts [l*per, (l+1)*per); exclusive warp scans
+  const int per = ceil_div(E, 32);
+  const int e0 = min(E, lane * per), e1 = min(E, e0 + per);
+  int run = 0, arun = 0;
+  for (int e2 = e0; e2 < e1; ++e2) {
+    const int pc = tab[e2];
+    run += pc;
+    arun += pc > 0;
+  }
+  int incl = run, aincl = arun;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    const int ya = __shfl_up_sync(0xffffffffu, aincl, o);
+    if (lane >= o) {
+      incl += y;
+      aincl += ya;
     }
   }
+  int off = incl - run, aoff = aincl - arun;
+  for (int e2 = e0; e2 < e1; ++e2) {
+    const int pc = tab[e2];
+    p.offsets[e2] = off;
+    p.counts[e2] = 0;
+    offs[e2] = off;
+    aidx[e2] = aoff;
+    off += pc;
+    aoff += pc > 0;
+  }
+  const int n_pad = __shfl_sync(0xffffffffu, incl, 31);
+  __syncwarp();
   if (valid) {
-    const int pos = before + within;
+    const int pos = offs[e] + within;
     BEAM_DCHECK(p, p.cap == 0 || (pos >= 0 && pos < p.cap), kChkPlanPos);
     const int t = lane / K;
     p.tok[pos] = t;
@@ -629,39 +653,17 @@ __device__ __forceinline__ void plan_warp(const int32_t* ids, const float* w, in
     if (p.slot_expert) p.slot_expert[lane] = -1;
   }
   if (leader) {
-    p.active[act_before] = e;
-    if (pad)
+    p.active[aidx[e]] = e;
+    p.counts[e] = cnt;  // after the zero fill (same lane order: the zero fill above precedes this store)
+    if (pad) {
+      const int before = offs[e];
       for (int q = before + cnt; q < before + padded; ++q) {
         p.tok[q] = -1;
         p.slot[q] = -1;
         if (p.w) p.w[q] = 0.0f;
       }
+    }
   }
-  const int n_act = __popc(__ballot_sync(0xffffffffu, leader));
-  const int n_real = __popc(__ballot_sync(0xffffffffu, valid));
-  __syncwarp();
-  // counts / padded offsets of every expert (inactive: count 0): lane l owns the
-  // contiguous experts [l*per, (l+1)*per); exclusive warp scan of their sums
-  const int per = ceil_div(E, 32);
-  const int e0 = min(E, lane * per), e1 = min(E, e0 + per);
-  int run = 0;
-  for (int e2 = e0; e2 < e1; ++e2) run += tab[e2];
-  int incl = run;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  int off = incl - run;
-  for (int e2 = e0; e2 < e1; ++e2) {
-    const int pc = tab[e2];
-    p.offsets[e2] = off;
-    p.counts[e2] = 0;
-    off += pc;
-  }
-  const int n_pad = __shfl_sync(0xffffffffu, incl, 31);
-  __syncwarp();
-  if (leader) p.counts[e] = cnt;  // after the zero fill (same warp, ordered by __syncwarp)
   if (lane == 0) {
     p.offsets[E] = n_pad;
     p.meta[0] = n_act;
