@@ -245,7 +245,16 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
                                            const TopkArgs& a) {
   const int N = a.N, Nr = KIND == BEAM_ROUTE_BEAM ? a.N : a.Nr;
   float inv = 1.0f;
-  if (a.has_norm && a.ss_part != nullptr) {  // split partials from the projection CTAs
+  // split partials of sum(x^2) from the projection CTAs (the fused gate): loaded
+  // here, summed after the logit partials below are issued — one L2 round trip
+  // for both instead of two
+  const bool ss_split = a.has_norm && a.ss_part != nullptr;
+  float ssv[CG ? MAXSPLIT : 1];
+  if (CG && ss_split) {
+#pragma unroll
+    for (int sp = 0; sp < (CG ? MAXSPLIT : 1); ++sp)
+      ssv[sp] = ld_maybe_cg<CG>(a.ss_part + (size_t)min(sp, splits - 1) * T + t);
+  } else if (ss_split) {
     float ss = 0.0f;
 #pragma unroll
     for (int sp = 0; sp < MAXSPLIT; ++sp) {
@@ -299,7 +308,6 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
     ss = warp_sum(ss);
     inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
   }
-  if (a.inv_out && lane == 0) a.inv_out[t] = inv;
 
   // router logits v / mask pre-activations av of this lane's columns j = lane + 32 i,
   // summed over the split-K partials in split order
@@ -340,6 +348,13 @@ __device__ __forceinline__ void topk_token(const float* __restrict__ L, int spli
         }
     }
   }
+  if (CG && ss_split) {  // tensor.py:485-487 from the split partials, in split order
+    float ss = 0.0f;
+#pragma unroll
+    for (int sp = 0; sp < (CG ? MAXSPLIT : 1); ++sp) ss += sp < splits ? ssv[sp] : 0.0f;
+    inv = 1.0f / sqrtf(ss / (float)a.d + 1e-6f);
+  }
+  if (a.inv_out && lane == 0) a.inv_out[t] = inv;
   topk_finish<NPL, KIND>(v, av, inv, t, lane, a);
 }
 
