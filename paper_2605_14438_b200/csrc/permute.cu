@@ -75,12 +75,16 @@ __global__ void __launch_bounds__(kMcThreads) permute_hist_kernel(const IdT* __r
     for (int q = 0; q < kMcWarps; ++q) c += sh[q * E + e];
     hist_g[(size_t)blockIdx.x * E + e] = c;
   }
-  __threadfence();
+  // handoff: CTA barrier, then one acq_rel (gpu scope, cumulative) increment by
+  // thread 0; the last CTA's increment acquires every CTA's histogram
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
+  if (tid == 0) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(counter) : "memory");
+    s_last = old == (int)gridDim.x - 1;
+  }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   const int G = gridDim.x;
   if (tid == 0) carry[0] = carry[1] = carry[2] = 0;
   __syncthreads();
