@@ -234,14 +234,17 @@ __device__ __forceinline__ void router_gemv_body(const TX* __restrict__ X, const
       q = warp_sum(q);
       if (lane == 0) ssp[(size_t)split * T + t0 + t] = q;
     }
-    if (xw != nullptr) {
-      // the norm-weighted token rows x * w (fp32, exactly the product the decode
-      // gate/up kernels formed per chunk) for the expert stage: its inner loop
-      // then loads one row per token and does no per-chunk norm multiply; a bf16
-      // copy right behind them ([T, d_pad] after the fp32 rows) feeds the
-      // tensor-core items as one MMA operand
+  }
+  if (ssp != nullptr && xw != nullptr) {
+    // the norm-weighted token rows x * w (fp32, exactly the product the decode
+    // gate/up kernels formed per chunk) for the expert stage: its inner loop
+    // then loads one row per token and does no per-chunk norm multiply; a bf16
+    // copy right behind them ([T, d_pad] after the fp32 rows) feeds the
+    // tensor-core items as one MMA operand.  Spread over the tile's column CTAs
+    // (they all hold the token tile), so no CTA's projection waits on all of it.
+    {
       __nv_bfloat16* xw16 = reinterpret_cast<__nv_bfloat16*>(xw + (size_t)T * d_pad);
-      for (int v = threadIdx.x; v < nt * (kn >> 2); v += 256) {
+      for (int v = threadIdx.x + 256 * blockIdx.x; v < nt * (kn >> 2); v += 256 * gridDim.x) {
         const int t = v / (kn >> 2), k4 = v % (kn >> 2);
         const float4 x = *reinterpret_cast<const float4*>(xs + t * kr + 4 * k4);
         const float4 g = ld_norm4(nw, ks + 4 * k4, d);
